@@ -1,0 +1,159 @@
+/*
+ * tnx.h -- C ABI of the B200 sliced contraction-tree executor (libtnx.so).
+ *
+ * The reference (arXiv 2002.01935, package `hypertn`) is pure Python and has
+ * no FFI; its hot-path entry points are the SPEC executor signatures
+ *
+ *   contract(tn, tree, options{strip_exponent})
+ *   contract_sliced(tn, tree, slice_set, options)
+ *
+ * built from ContractionTree (pkg/src/hypertn/tree.py:32), annotate_incidence
+ * (tree.py:137), pairwise_contract (dense.py:61) and fix_index (dense.py:161).
+ * This header is the native boundary those Python signatures bind to
+ * (paper_2002_01935_b200/_native.py; the ctypes stub a maintainer would add
+ * on the reference side is in INTEGRATION.md).  Everything crossing it is a
+ * plain pointer + size; no exceptions cross it: every call returns a
+ * tnx_status and tnx_last_error() gives the thread-local message.
+ *
+ * Ownership: the caller owns leaf data (host or device pointers, complex128
+ * or complex64, row-major in the leaf's label order); the library owns the
+ * plan, its HBM arenas, CUDA graph and device accumulator.  One plan drives
+ * one device; plans for different devices may be used concurrently from
+ * different host threads; calls on one plan must be serialised.
+ */
+#ifndef TNX_H_
+#define TNX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TNX_OK = 0,
+  TNX_ERR_INVALID = 1,   /* ValueError in the reference (tree.py:43-56, dense.py:73/166) */
+  TNX_ERR_DATA = 2,      /* DataError (network.py:18-19) */
+  TNX_ERR_CUDA = 3,      /* CUDA runtime / driver failure */
+  TNX_ERR_OOM = 4,       /* arena does not fit the device */
+  TNX_ERR_NUMERIC = 5,   /* non-finite intermediate */
+  TNX_ERR_STATE = 6      /* call out of order (e.g. run before bind) */
+} tnx_status;
+
+typedef enum {
+  TNX_PREC_FP32 = 0,     /* every contraction on FP32 SIMT kernels */
+  TNX_PREC_3XTF32 = 1    /* GEMM-shaped contractions on tcgen05 tensor cores,
+                            split-TF32 (hi*hi + hi*lo + lo*hi), 4M complex,
+                            FP32 accumulation in TMEM; the rest FP32 SIMT */
+} tnx_precision;
+
+/* Leaf data element type / location for tnx_bind_leaves. */
+enum { TNX_DTYPE_C128 = 0, TNX_DTYPE_C64 = 1 };
+enum { TNX_LOC_HOST = 0, TNX_LOC_DEVICE = 1 };
+
+/* Plan flags. */
+enum {
+  TNX_FLAG_NO_GRAPH = 1u << 0,   /* launch per-slice steps directly (debug) */
+  TNX_FLAG_NO_HOIST = 1u << 1    /* recompute slice-invariant subtrees per slice */
+};
+
+/*
+ * Network + tree + slice set, interned.  Labels are integer ids 0..L-1 in the
+ * reference's interning order (tn.index_table order, hypergraph.py:41-43).
+ * Leaves are listed in SSA leaf order: leaf i is network node tree.leaves[i]
+ * (tree.py:37-57).  pairs holds the n-1 SSA merges (a_k, b_k), merge k
+ * creating vertex n+k.  sliced_labels is the SliceSet label order; slice id
+ * s enumerates its assignments mixed-radix, last label fastest.
+ */
+typedef struct {
+  int32_t num_labels;
+  const int64_t* label_dims;        /* [num_labels] */
+  int32_t num_leaves;
+  const int32_t* leaf_ranks;        /* [num_leaves] */
+  const int32_t* leaf_labels;       /* concatenated, sum(leaf_ranks) */
+  const int32_t* pairs;             /* [2*(num_leaves-1)] */
+  int32_t num_output;
+  const int32_t* output_labels;     /* tn.output order */
+  int32_t num_sliced;
+  const int32_t* sliced_labels;
+  int32_t precision;                /* tnx_precision */
+  int32_t device;                   /* CUDA ordinal */
+  uint32_t flags;
+  int32_t reserved;
+  double gemm_min_macs;             /* 0 -> library default */
+} tnx_plan_desc;
+
+typedef struct {
+  uint64_t op_count_lo, op_count_hi;   /* per-slice MACs  sum_v U_v (128-bit) */
+  uint64_t d_lo, d_hi;                 /* d_sliced (128-bit) */
+  double width;                        /* W_s = log2 max internal size */
+  uint64_t peak_elements;              /* 2^W_s */
+  uint64_t work_arena_bytes;
+  uint64_t persistent_bytes;
+  uint64_t leaf_bytes;
+  int32_t num_vertices;                /* internal vertices */
+  int32_t num_hoisted;                 /* slice-invariant internal vertices */
+  int32_t num_gemm;                    /* per-slice vertices on tcgen05 */
+  int32_t num_simt;                    /* per-slice vertices on SIMT kernels */
+  int32_t launches_per_slice;          /* kernels launched per slice */
+  int32_t out_rank;
+  int64_t out_elements;
+} tnx_stats;
+
+/* Per internal vertex description (introspection / tests). */
+typedef struct {
+  int32_t ssa;               /* vertex id n+k */
+  int32_t kind;              /* 0 SIMT thread/out, 1 SIMT warp/out, 2 SIMT split, 3 GEMM */
+  int32_t hoisted;           /* computed once per bind */
+  int32_t rank;              /* rank of the result */
+  int64_t m, n, k, batch;    /* GEMM-view extents */
+  uint64_t macs_lo, macs_hi; /* U_v */
+} tnx_vertex_info;
+
+const char* tnx_last_error(void);
+const char* tnx_version(void);
+
+/* Compile bookkeeping, kernel choice and the HBM arena plan.  No device
+ * memory is touched until tnx_bind_leaves.  */
+int tnx_plan_create(const tnx_plan_desc* desc, void** plan_out);
+int tnx_plan_destroy(void* plan);
+
+/* Upload the leaves (one pointer per SSA leaf), allocate the arenas, compute
+ * the slice-invariant subtrees once, capture the per-slice CUDA graph and
+ * zero the accumulator.  stream may be NULL (library stream). */
+int tnx_bind_leaves(void* plan, const void* const* leaf_data, int32_t dtype,
+                    int32_t location, void* stream);
+
+/* Contract slices [s_begin, s_end) and add them (compensated, complex128)
+ * into the device accumulator.  Asynchronous on `stream`. */
+int tnx_run_slices(void* plan, uint64_t s_begin, uint64_t s_end, void* stream);
+
+int tnx_reset_accumulator(void* plan, void* stream);
+
+/* Copy the accumulator (complex128 interleaved, tn.output order) to host;
+ * synchronises `stream`.  out_elems must equal stats.out_elements. */
+int tnx_partial_result(void* plan, double* out, int64_t out_elems, void* stream);
+
+int tnx_stats_get(void* plan, tnx_stats* out);
+int tnx_vertex_info_get(void* plan, int32_t index, tnx_vertex_info* out);
+
+/* Debug/parity: run slice s up to and including SSA vertex v (which must be
+ * slice-dependent or hoisted) and copy its complex64 result to host together
+ * with its memory layout (label ids, row-major).  */
+int tnx_debug_vertex(void* plan, uint64_t s, int32_t v, float* out_c64,
+                     int64_t out_elems, int32_t* layout_labels, int32_t* rank_out);
+
+/* Synchronise the plan's device; returns a CUDA error if one is pending. */
+int tnx_synchronize(void* plan);
+
+/* Standalone kernels exposed for unit tests / micro-benchmarks (device
+ * pointers).  C[b,m,n] = sum_k A[b,m,k] B[b,n,k] over complex64 with the
+ * tcgen05 split-TF32 path (A, B row-major, K innermost). */
+int tnx_gemm_c64(const void* A, const void* B, void* C, int64_t batch, int64_t M,
+                 int64_t N, int64_t K, int32_t precision, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TNX_H_ */

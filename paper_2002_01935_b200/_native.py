@@ -1,0 +1,115 @@
+"""ctypes binding of libtnx.so (C ABI declared in include/tnx.h).
+
+The product path fails loudly when the library is missing: there is no CPU
+fallback anywhere in this package.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libtnx.so")
+
+TNX_OK, TNX_ERR_INVALID, TNX_ERR_DATA, TNX_ERR_CUDA, TNX_ERR_OOM, TNX_ERR_NUMERIC, TNX_ERR_STATE = range(7)
+PREC_FP32, PREC_3XTF32 = 0, 1
+DTYPE_C128, DTYPE_C64 = 0, 1
+LOC_HOST, LOC_DEVICE = 0, 1
+FLAG_NO_GRAPH, FLAG_NO_HOIST = 1, 2
+
+KIND_NAMES = {0: "simt_thread", 1: "simt_warp", 2: "simt_split", 3: "gemm_tc"}
+
+
+class PlanDesc(C.Structure):
+    _fields_ = [
+        ("num_labels", C.c_int32), ("label_dims", C.POINTER(C.c_int64)),
+        ("num_leaves", C.c_int32), ("leaf_ranks", C.POINTER(C.c_int32)),
+        ("leaf_labels", C.POINTER(C.c_int32)), ("pairs", C.POINTER(C.c_int32)),
+        ("num_output", C.c_int32), ("output_labels", C.POINTER(C.c_int32)),
+        ("num_sliced", C.c_int32), ("sliced_labels", C.POINTER(C.c_int32)),
+        ("precision", C.c_int32), ("device", C.c_int32), ("flags", C.c_uint32),
+        ("reserved", C.c_int32), ("gemm_min_macs", C.c_double),
+    ]
+
+
+class Stats(C.Structure):
+    _fields_ = [
+        ("op_count_lo", C.c_uint64), ("op_count_hi", C.c_uint64),
+        ("d_lo", C.c_uint64), ("d_hi", C.c_uint64),
+        ("width", C.c_double), ("peak_elements", C.c_uint64),
+        ("work_arena_bytes", C.c_uint64), ("persistent_bytes", C.c_uint64),
+        ("leaf_bytes", C.c_uint64),
+        ("num_vertices", C.c_int32), ("num_hoisted", C.c_int32),
+        ("num_gemm", C.c_int32), ("num_simt", C.c_int32),
+        ("launches_per_slice", C.c_int32), ("out_rank", C.c_int32),
+        ("out_elements", C.c_int64),
+    ]
+
+
+class VertexInfo(C.Structure):
+    _fields_ = [
+        ("ssa", C.c_int32), ("kind", C.c_int32), ("hoisted", C.c_int32), ("rank", C.c_int32),
+        ("m", C.c_int64), ("n", C.c_int64), ("k", C.c_int64), ("batch", C.c_int64),
+        ("macs_lo", C.c_uint64), ("macs_hi", C.c_uint64),
+    ]
+
+
+# every symbol include/tnx.h declares, with its ctypes signature
+SIGNATURES = {
+    "tnx_last_error": (C.c_char_p, []),
+    "tnx_version": (C.c_char_p, []),
+    "tnx_plan_create": (C.c_int, [C.POINTER(PlanDesc), C.POINTER(C.c_void_p)]),
+    "tnx_plan_destroy": (C.c_int, [C.c_void_p]),
+    "tnx_bind_leaves": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_void_p]),
+    "tnx_run_slices": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]),
+    "tnx_reset_accumulator": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "tnx_partial_result": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_int64, C.c_void_p]),
+    "tnx_stats_get": (C.c_int, [C.c_void_p, C.POINTER(Stats)]),
+    "tnx_vertex_info_get": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(VertexInfo)]),
+    "tnx_debug_vertex": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int32, C.POINTER(C.c_float), C.c_int64,
+                                   C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "tnx_synchronize": (C.c_int, [C.c_void_p]),
+    "tnx_gemm_c64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
+                               C.c_int64, C.c_int32, C.c_void_p]),
+}
+
+_lib = None
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"libtnx error {code}: {msg}")
+        self.code = code
+
+
+def load():
+    """Load libtnx.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} missing: build it with "
+                           "`python -m paper_2002_01935_b200.build` (no CPU fallback exists)")
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc):
+    if rc != TNX_OK:
+        msg = load().tnx_last_error().decode(errors="replace")
+        if rc in (TNX_ERR_INVALID, TNX_ERR_STATE):
+            raise ValueError(msg)
+        if rc == TNX_ERR_DATA:
+            from .network import DataError
+            raise DataError(msg)
+        if rc == TNX_ERR_NUMERIC:
+            raise FloatingPointError(msg)
+        if rc == TNX_ERR_OOM:
+            raise MemoryError(msg)
+        raise NativeError(rc, msg)

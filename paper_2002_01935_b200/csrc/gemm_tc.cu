@@ -1,0 +1,382 @@
+// K3: tcgen05 / TMEM / TMA complex64 GEMM with split-TF32 (3 passes) and the
+// 4M complex decomposition, for the GEMM-shaped pairwise contractions of the
+// tree (reference pairwise_contract -> np.einsum -> zgemm, dense.py:47-76).
+//
+//   C[b,m,n] = sum_k A[b,m,k] * B[b,n,k]          (complex64 in/out)
+//
+// Operands arrive as four fp32 planes each ([re_hi, re_lo, im_hi, im_lo],
+// [batch*rows][kp] K-major, written by the pack kernel).  Per 8-wide k-step
+// one elected thread issues 12 tcgen05.mma.kind::tf32 (M=128, N=128, K=8):
+//
+//   Cre += Ar_h Br_h + Ar_h Br_l + Ar_l Br_h - (Ai_h Bi_h + Ai_h Bi_l + Ai_l Bi_h)
+//   Cim += Ar_h Bi_h + Ar_h Bi_l + Ar_l Bi_h +  Ai_h Br_h + Ai_h Br_l + Ai_l Br_h
+//
+// (the minus uses the instruction descriptor's negate-A bit), accumulating
+// in two FP32 TMEM accumulators (256 columns).  A warp-specialised mbarrier
+// pipeline (TMA producer / MMA issuer) streams 3 stages of 64 KB; the
+// epilogue moves TMEM -> registers (tcgen05.ld) -> interleaved complex64.
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include "tnx_kernels.h"
+
+namespace tnx {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 128;
+constexpr int BK = 16;                          // fp32 per smem row (64 B, SWIZZLE_64B)
+constexpr int STAGES = 3;
+constexpr int PLANE_BYTES = BM * BK * 4;        // 8 KB per plane tile
+constexpr int STAGE_BYTES = 8 * PLANE_BYTES;    // 4 A planes + 4 B planes
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int TMEM_COLS = 256;
+constexpr int GROUP_M = 8;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, uint32_t mbar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(mbar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_64B, rows of 64 B,
+// 8-row groups 512 B apart (SBO), LBO unused (=1), sm100 version bit.
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;
+  d |= (uint64_t)(512u >> 4) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)4u << 61;
+  return d;
+}
+
+// Instruction descriptor: D=f32, A=B=tf32, K-major both, N=128, M=128.
+__host__ __device__ constexpr uint32_t idesc_tf32(bool neg_a) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((neg_a ? 1u : 0u) << 13) |
+         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint32_t mbar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+struct GemmArgs {
+  float2* out;
+  int64_t M, N, batch;
+  int32_t num_kb;        // kp / BK
+  int32_t tiles_m, tiles_n;
+  int64_t rows_a, rows_b;  // batch * M, batch * N (rows per plane)
+};
+
+__global__ void __launch_bounds__(128, 1)
+    gemm_c64_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a,
+                           const __grid_constant__ CUtensorMap tm_b, const GemmArgs g) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  // bars[0..S) full, bars[S..2S) empty, bars[2S] done; tmem slot after
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  // grouped rasterisation of the (m, n) tile grid for L2 reuse
+  const int tile = blockIdx.x;
+  const int group_span = GROUP_M * g.tiles_n;
+  const int group = tile / group_span;
+  const int first_m = group * GROUP_M;
+  const int gm = min(g.tiles_m - first_m, GROUP_M);
+  const int tm = first_m + (tile % group_span) % gm;
+  const int tn = (tile % group_span) / gm;
+  const int b = blockIdx.y;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_addr(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_addr(&bars[s]), 1);
+      mbar_init(smem_addr(&bars[STAGES + s]), 1);
+    }
+    mbar_init(smem_addr(&bars[2 * STAGES]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int nkb = g.num_kb;
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer ----------------
+    const int row_a = (int)(b * g.M + (int64_t)tm * BM);
+    const int row_b = (int)(b * g.N + (int64_t)tn * BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      mbar_wait(smem_addr(&bars[STAGES + stage]), phase ^ 1u);
+      const uint32_t full = smem_addr(&bars[stage]);
+      mbar_expect_tx(full, STAGE_BYTES);
+      unsigned char* sbase = smem + stage * STAGE_BYTES;
+      const int kc = kb * BK;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        tma_load_2d(smem_addr(sbase + p * PLANE_BYTES), &tm_a, full, kc,
+                    (int)(p * g.rows_a + row_a));
+        tma_load_2d(smem_addr(sbase + (4 + p) * PLANE_BYTES), &tm_b, full, kc,
+                    (int)(p * g.rows_b + row_b));
+      }
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t d_re = tmem_base;
+    const uint32_t d_im = tmem_base + BN;
+    constexpr uint32_t ID_POS = idesc_tf32(false);
+    constexpr uint32_t ID_NEG = idesc_tf32(true);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      mbar_wait(smem_addr(&bars[stage]), phase);
+      tc_fence_after();
+      const uint32_t sb = smem_addr(smem + stage * STAGE_BYTES);
+#pragma unroll
+      for (int ks = 0; ks < BK / 8; ++ks) {
+        const uint32_t koff = ks * 32;  // bytes within the 64 B swizzled row
+        const uint64_t ar_h = umma_desc_sw64(sb + 0 * PLANE_BYTES + koff);
+        const uint64_t ar_l = umma_desc_sw64(sb + 1 * PLANE_BYTES + koff);
+        const uint64_t ai_h = umma_desc_sw64(sb + 2 * PLANE_BYTES + koff);
+        const uint64_t ai_l = umma_desc_sw64(sb + 3 * PLANE_BYTES + koff);
+        const uint64_t br_h = umma_desc_sw64(sb + 4 * PLANE_BYTES + koff);
+        const uint64_t br_l = umma_desc_sw64(sb + 5 * PLANE_BYTES + koff);
+        const uint64_t bi_h = umma_desc_sw64(sb + 6 * PLANE_BYTES + koff);
+        const uint64_t bi_l = umma_desc_sw64(sb + 7 * PLANE_BYTES + koff);
+        const uint32_t acc0 = (kb | ks) ? 1u : 0u;
+        // small cross terms first
+        umma_tf32(d_re, ar_h, br_l, ID_POS, acc0);
+        umma_tf32(d_re, ar_l, br_h, ID_POS, 1u);
+        umma_tf32(d_re, ai_h, bi_l, ID_NEG, 1u);
+        umma_tf32(d_re, ai_l, bi_h, ID_NEG, 1u);
+        umma_tf32(d_re, ar_h, br_h, ID_POS, 1u);
+        umma_tf32(d_re, ai_h, bi_h, ID_NEG, 1u);
+        umma_tf32(d_im, ar_h, bi_l, ID_POS, acc0);
+        umma_tf32(d_im, ar_l, bi_h, ID_POS, 1u);
+        umma_tf32(d_im, ai_h, br_l, ID_POS, 1u);
+        umma_tf32(d_im, ai_l, br_h, ID_POS, 1u);
+        umma_tf32(d_im, ar_h, bi_h, ID_POS, 1u);
+        umma_tf32(d_im, ai_h, br_h, ID_POS, 1u);
+      }
+      umma_commit(smem_addr(&bars[STAGES + stage]));  // frees the smem stage
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+    umma_commit(smem_addr(&bars[2 * STAGES]));  // accumulators complete
+  }
+  __syncwarp();
+
+  // ---------------- epilogue: TMEM -> registers -> complex64 ----------------
+  mbar_wait(smem_addr(&bars[2 * STAGES]), 0);
+  tc_fence_after();
+  const int64_t row = (int64_t)tm * BM + warp * 32 + lane;
+  const uint32_t lane_base = tmem_base + ((uint32_t)(warp * 32) << 16);
+  float2* orow = g.out + ((int64_t)b * g.M + row) * g.N;
+  const bool row_ok = row < g.M;
+#pragma unroll 1
+  for (int c = 0; c < BN; c += 16) {
+    uint32_t re[16], im[16];
+    tmem_ld16(lane_base + c, re);
+    tmem_ld16(lane_base + BN + c, im);
+    tmem_wait_ld();
+    const int64_t col = (int64_t)tn * BN + c;
+    if (row_ok) {
+      if (col + 16 <= g.N && (g.N & 1) == 0) {
+        float4* dst = reinterpret_cast<float4*>(orow + col);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          dst[j] = make_float4(__uint_as_float(re[2 * j]), __uint_as_float(im[2 * j]),
+                               __uint_as_float(re[2 * j + 1]), __uint_as_float(im[2 * j + 1]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (col + j < g.N) orow[col + j] = make_float2(__uint_as_float(re[j]), __uint_as_float(im[j]));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode(char* err, size_t errlen) {
+  static EncodeTiledFn fn = nullptr;
+  if (fn) return fn;
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+  if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !p) {
+    snprintf(err, errlen, "cuTensorMapEncodeTiled unavailable (%s)", cudaGetErrorString(e));
+    return nullptr;
+  }
+  fn = reinterpret_cast<EncodeTiledFn>(p);
+  return fn;
+}
+
+int encode_planes(void* tmap, const float* base, int64_t rows_total, int64_t kp, char* err,
+                  size_t errlen) {
+  EncodeTiledFn enc = get_encode(err, errlen);
+  if (!enc) return 1;
+  cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows_total};
+  cuuint64_t strides[1] = {(cuuint64_t)(kp * 4)};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)BM};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(reinterpret_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                   const_cast<float*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    snprintf(err, errlen, "cuTensorMapEncodeTiled failed (CUresult %d, rows %lld kp %lld)", (int)r,
+             (long long)rows_total, (long long)kp);
+    return 1;
+  }
+  return 0;
+}
+
+}  // namespace
+
+int gemm_init_attributes(char* err, size_t errlen) {
+  cudaError_t e = cudaFuncSetAttribute(gemm_c64_3xtf32_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (e != cudaSuccess) {
+    snprintf(err, errlen, "cudaFuncSetAttribute(gemm): %s", cudaGetErrorString(e));
+    return 1;
+  }
+  return 0;
+}
+
+int gemm_prepare(GemmPlan* g, const float* a_planes, const float* b_planes, float2* out,
+                 int64_t batch, int64_t M, int64_t N, int64_t kp, char* err, size_t errlen) {
+  std::memset(g, 0, sizeof(*g));
+  if (kp % BK != 0) {
+    snprintf(err, errlen, "gemm: kp=%lld not a multiple of %d", (long long)kp, BK);
+    return 1;
+  }
+  if (4 * batch * (M > N ? M : N) >= (int64_t(1) << 31)) {
+    snprintf(err, errlen, "gemm: row coordinate exceeds int32");
+    return 1;
+  }
+  if (encode_planes(g->tmap_a, a_planes, 4 * batch * M, kp, err, errlen)) return 1;
+  if (encode_planes(g->tmap_b, b_planes, 4 * batch * N, kp, err, errlen)) return 1;
+  g->out = out;
+  g->M = M;
+  g->N = N;
+  g->kp = kp;
+  g->batch = batch;
+  g->ok = 1;
+  return 0;
+}
+
+cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
+  GemmArgs a;
+  a.out = g.out;
+  a.M = g.M;
+  a.N = g.N;
+  a.batch = g.batch;
+  a.num_kb = (int32_t)(g.kp / BK);
+  a.tiles_m = (int32_t)((g.M + BM - 1) / BM);
+  a.tiles_n = (int32_t)((g.N + BN - 1) / BN);
+  a.rows_a = g.batch * g.M;
+  a.rows_b = g.batch * g.N;
+  dim3 grid((unsigned)(a.tiles_m * a.tiles_n), (unsigned)g.batch);
+  const CUtensorMap* ta = reinterpret_cast<const CUtensorMap*>(g.tmap_a);
+  const CUtensorMap* tb = reinterpret_cast<const CUtensorMap*>(g.tmap_b);
+  gemm_c64_3xtf32_kernel<<<grid, 128, SMEM_BYTES, st>>>(*ta, *tb, a);
+  return cudaGetLastError();
+}
+
+}  // namespace tnx

@@ -1,0 +1,312 @@
+// SIMT kernels of the sliced contraction executor (sm_100a).
+//
+//  K1 gather  : fix_index of every slice-dependent leaf for the current slice
+//               id (reference dense.py:161-170), read from a device counter so
+//               the per-slice CUDA graph needs no host update.
+//  K4 simt    : generic strided pairwise contraction (reference
+//               pairwise_contract, dense.py:61-76) in FP32 complex:
+//               thread-per-output, warp-per-output (lane-split sum, shuffle
+//               reduce) and split-reduction (block partials + finalize) modes.
+//  K2 pack    : permute a complex64 tensor into the four split-TF32 planes the
+//               tcgen05 GEMM consumes (coalesced along the padded K axis).
+//  K6 accum   : root -> tn.output order, Kahan-compensated complex128
+//               accumulation across slices.
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "tnx_kernels.h"
+
+namespace tnx {
+
+__device__ __forceinline__ void decode2(const IdxMap& m, int64_t idx, int64_t& o0, int64_t& o1) {
+#pragma unroll 1
+  for (int i = m.n - 1; i >= 0; --i) {
+    int64_t r;
+    if (m.lg[i] >= 0) {
+      r = idx & (m.dim[i] - 1);
+      idx >>= m.lg[i];
+    } else {
+      int64_t q = idx / m.dim[i];
+      r = idx - q * m.dim[i];
+      idx = q;
+    }
+    o0 += r * m.st0[i];
+    o1 += r * m.st1[i];
+  }
+}
+
+__device__ __forceinline__ void decode1(const IdxMap& m, int64_t idx, int64_t& o0) {
+#pragma unroll 1
+  for (int i = m.n - 1; i >= 0; --i) {
+    int64_t r;
+    if (m.lg[i] >= 0) {
+      r = idx & (m.dim[i] - 1);
+      idx >>= m.lg[i];
+    } else {
+      int64_t q = idx / m.dim[i];
+      r = idx - q * m.dim[i];
+      idx = q;
+    }
+    o0 += r * m.st0[i];
+  }
+}
+
+__device__ __forceinline__ void cfma(float2& acc, float2 a, float2 b) {
+  acc.x = fmaf(a.x, b.x, acc.x);
+  acc.x = fmaf(-a.y, b.y, acc.x);
+  acc.y = fmaf(a.x, b.y, acc.y);
+  acc.y = fmaf(a.y, b.x, acc.y);
+}
+
+// ------------------------------------------------------------------ gather
+__global__ void gather_kernel(const GatherJob* __restrict__ jobs, const float2* __restrict__ pool,
+                              const unsigned long long* __restrict__ counter) {
+  const GatherJob& j = jobs[blockIdx.x];
+  const unsigned long long s = *counter;
+  int64_t base = j.src;
+  for (int i = 0; i < j.n_sl; ++i) {
+    unsigned long long digit = (s / j.radix[i]) % (unsigned long long)j.sdim[i];
+    base += (int64_t)digit * j.sst[i];
+  }
+  for (int64_t e = threadIdx.x; e < j.out_size; e += blockDim.x) {
+    int64_t off = base, idx = e;
+    for (int i = j.n_kept - 1; i >= 0; --i) {
+      int64_t q = idx / j.kdim[i];
+      off += (idx - q * j.kdim[i]) * j.kst[i];
+      idx = q;
+    }
+    j.dst[e] = pool[off];
+  }
+}
+
+cudaError_t launch_gather(const GatherJob* jobs, int njobs, const float2* pool,
+                          const unsigned long long* counter, cudaStream_t st) {
+  if (njobs == 0) return cudaSuccess;
+  gather_kernel<<<njobs, 64, 0, st>>>(jobs, pool, counter);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ simt
+__global__ void __launch_bounds__(256) simt_thread_kernel(const SimtParams p) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < p.out_size; o += stride) {
+    int64_t ox = 0, oy = 0;
+    decode2(p.out, o, ox, oy);
+    float2 acc = make_float2(0.f, 0.f);
+    if (p.sum_tab) {
+      for (int64_t j = 0; j < p.sum_size; ++j) {
+        Int2Off t = p.sum_tab[j];
+        cfma(acc, p.x[ox + t.x], p.y[oy + t.y]);
+      }
+    } else {
+      for (int64_t j = 0; j < p.sum_size; ++j) {
+        int64_t sx = ox, sy = oy;
+        decode2(p.sum, j, sx, sy);
+        cfma(acc, p.x[sx], p.y[sy]);
+      }
+    }
+    p.z[o] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(256) simt_warp_kernel(const SimtParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t o = warp; o < p.out_size; o += nwarps) {
+    int64_t ox = 0, oy = 0;
+    decode2(p.out, o, ox, oy);
+    float2 acc = make_float2(0.f, 0.f);
+    if (p.sum_tab) {
+      for (int64_t j = lane; j < p.sum_size; j += 32) {
+        Int2Off t = p.sum_tab[j];
+        cfma(acc, p.x[ox + t.x], p.y[oy + t.y]);
+      }
+    } else {
+      for (int64_t j = lane; j < p.sum_size; j += 32) {
+        int64_t sx = ox, sy = oy;
+        decode2(p.sum, j, sx, sy);
+        cfma(acc, p.x[sx], p.y[sy]);
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+    }
+    if (lane == 0) p.z[o] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(256) simt_split_kernel(const SimtParams p) {
+  // grid: (nsplit, out_size)
+  const int64_t o = blockIdx.y;
+  const int64_t j0 = (int64_t)blockIdx.x * p.chunk;
+  const int64_t j1 = min(j0 + p.chunk, p.sum_size);
+  int64_t ox = 0, oy = 0;
+  decode2(p.out, o, ox, oy);
+  float2 acc = make_float2(0.f, 0.f);
+  for (int64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+    int64_t sx = ox, sy = oy;
+    decode2(p.sum, j, sx, sy);
+    cfma(acc, p.x[sx], p.y[sy]);
+  }
+  __shared__ float2 red[32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int nw = blockDim.x >> 5;
+    float2 v = threadIdx.x < nw ? red[threadIdx.x] : make_float2(0.f, 0.f);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      v.x += __shfl_xor_sync(0xffffffffu, v.x, off);
+      v.y += __shfl_xor_sync(0xffffffffu, v.y, off);
+    }
+    if (threadIdx.x == 0) p.partial[o * p.nsplit + blockIdx.x] = v;
+  }
+}
+
+__global__ void simt_finalize_kernel(const float2* __restrict__ partial, float2* __restrict__ z,
+                                     int64_t out_size, int nsplit) {
+  const int64_t o = blockIdx.x;
+  double re = 0.0, im = 0.0;
+  for (int i = threadIdx.x; i < nsplit; i += blockDim.x) {
+    float2 v = partial[o * nsplit + i];
+    re += v.x;
+    im += v.y;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    re += __shfl_xor_sync(0xffffffffu, re, off);
+    im += __shfl_xor_sync(0xffffffffu, im, off);
+  }
+  __shared__ double r2[64];
+  if ((threadIdx.x & 31) == 0) {
+    r2[threadIdx.x >> 5] = re;
+    r2[32 + (threadIdx.x >> 5)] = im;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a += r2[w];
+      b += r2[32 + w];
+    }
+    z[o] = make_float2((float)a, (float)b);
+  }
+}
+
+static int grid_for(int64_t work, int threads, int max_blocks) {
+  int64_t b = (work + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > max_blocks) b = max_blocks;
+  return (int)b;
+}
+
+cudaError_t launch_simt(const SimtParams& p, cudaStream_t st) {
+  if (p.out_size == 0) return cudaSuccess;
+  const int maxb = 148 * 16;
+  if (p.mode == SIMT_THREAD) {
+    simt_thread_kernel<<<grid_for(p.out_size, 256, maxb), 256, 0, st>>>(p);
+  } else if (p.mode == SIMT_WARP) {
+    simt_warp_kernel<<<grid_for(p.out_size * 32, 256, maxb), 256, 0, st>>>(p);
+  } else {
+    dim3 grid((unsigned)p.nsplit, (unsigned)p.out_size);
+    simt_split_kernel<<<grid, 256, 0, st>>>(p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    simt_finalize_kernel<<<(unsigned)p.out_size, 128, 0, st>>>(p.partial, p.z, p.out_size, p.nsplit);
+  }
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ pack
+__global__ void __launch_bounds__(256) pack_kernel(const PackParams p) {
+  const int64_t total = p.rows * p.kp;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int64_t r = e / p.kp;
+    const int64_t k = e - r * p.kp;
+    float re = 0.f, im = 0.f;
+    if (k < p.K) {
+      int64_t off = 0;
+      decode1(p.row, r, off);
+      decode1(p.col, k, off);
+      float2 v = p.src[off];
+      re = v.x;
+      im = v.y;
+    }
+    const float re_hi = __uint_as_float(__float_as_uint(re) & 0xffffe000u);
+    const float im_hi = __uint_as_float(__float_as_uint(im) & 0xffffe000u);
+    p.dst[e] = re_hi;
+    p.dst[e + p.plane_stride] = re - re_hi;
+    p.dst[e + 2 * p.plane_stride] = im_hi;
+    p.dst[e + 3 * p.plane_stride] = im - im_hi;
+  }
+}
+
+cudaError_t launch_pack(const PackParams& p, cudaStream_t st) {
+  pack_kernel<<<grid_for(p.rows * p.kp, 256, 148 * 32), 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ accumulate
+__global__ void accum_kernel(const AccumParams p) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t o = tid; o < p.out_size; o += stride) {
+    int64_t off = 0;
+    decode1(p.out, o, off);
+    double re = 0.0, im = 0.0;
+    for (int64_t e = 0; e < p.extra_size; ++e) {
+      int64_t eo = off;
+      decode1(p.extra, e, eo);
+      float2 v = p.root[eo];
+      re += v.x;
+      im += v.y;
+    }
+    // Kahan-compensated complex128 accumulation
+    double2 s = p.acc[o], c = p.comp[o];
+    double yr = re - c.x, yi = im - c.y;
+    double tr = s.x + yr, ti = s.y + yi;
+    c.x = (tr - s.x) - yr;
+    c.y = (ti - s.y) - yi;
+    p.acc[o] = make_double2(tr, ti);
+    p.comp[o] = c;
+  }
+  if (tid == 0 && p.slice_counter) *p.slice_counter += 1ull;
+}
+
+cudaError_t launch_accum(const AccumParams& p, cudaStream_t st) {
+  accum_kernel<<<grid_for(p.out_size, 256, 148 * 8), 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+__global__ void set_counter_kernel(unsigned long long* c, unsigned long long v) { *c = v; }
+
+cudaError_t launch_set_counter(unsigned long long* counter, unsigned long long v, cudaStream_t st) {
+  set_counter_kernel<<<1, 1, 0, st>>>(counter, v);
+  return cudaGetLastError();
+}
+
+__global__ void convert_kernel(const double2* __restrict__ s, float2* __restrict__ d, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    d[i] = make_float2((float)s[i].x, (float)s[i].y);
+}
+
+cudaError_t launch_convert_c128(const double2* src, float2* dst, int64_t n, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  convert_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(src, dst, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_zero(void* p, int64_t bytes, cudaStream_t st) {
+  return cudaMemsetAsync(p, 0, (size_t)bytes, st);
+}
+
+}  // namespace tnx

@@ -1,0 +1,1005 @@
+// libtnx: plan compiler, HBM arena planner and per-slice runtime of the B200
+// sliced contraction-tree executor.  C ABI in include/tnx.h.
+//
+// Reference semantics restated here (all citations /root/reference/...):
+//   * appearances = #carrier leaves + 1 if output   hypergraph.py:39-57
+//   * keep set of vertex v: labels whose accumulated leaf count is below the
+//     appearance count; order = survivors of a, then b's new labels
+//                                                   hypergraph.py:106-119,
+//                                                   tree.py:137-169
+//   * MACs per vertex = prod dims(s_a U s_b)        hypergraph.py:121-131
+//   * W = log2 max internal result size, C = sum    tree.py:172-190
+//   * slicing: sliced labels deleted from every incidence set, leaves
+//     projected with fix_index                      SPEC.md:463-482, dense.py:161-170
+//   * per pair: shared&kept = batch, shared&!kept = contracted,
+//     exclusive&!kept = single-operand sum          dense.py:61-76
+//   * slice ids: mixed radix over the SliceSet order, last label fastest
+//                                                   SURVEY.md §8(a) a14
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "tnx.h"
+#include "tnx_kernels.h"
+
+using namespace tnx;
+typedef unsigned __int128 u128;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define TNX_CUDA(call)                                                                  \
+  do {                                                                                  \
+    cudaError_t e__ = (call);                                                           \
+    if (e__ != cudaSuccess)                                                             \
+      return fail(TNX_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e__));   \
+  } while (0)
+
+namespace {
+
+constexpr int64_t kAlign = 256;
+inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct Block {
+  int64_t bytes = 0;
+  int first = 0, last = 0;
+  int64_t offset = 0;
+};
+
+// Greedy-by-size interval packing: largest blocks first, each placed at the
+// lowest offset that does not overlap a time-overlapping placed block.
+int64_t pack_blocks(std::vector<Block>& blocks) {
+  std::vector<int> order(blocks.size());
+  for (size_t i = 0; i < blocks.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return blocks[a].bytes > blocks[b].bytes; });
+  std::vector<int> placed;
+  int64_t total = 0;
+  for (int i : order) {
+    Block& bl = blocks[i];
+    std::vector<std::pair<int64_t, int64_t>> busy;
+    for (int j : placed) {
+      const Block& o = blocks[j];
+      if (o.last < bl.first || bl.last < o.first) continue;
+      busy.push_back({o.offset, o.offset + o.bytes});
+    }
+    std::sort(busy.begin(), busy.end());
+    int64_t off = 0;
+    for (auto& iv : busy) {
+      if (off + bl.bytes <= iv.first) break;
+      off = std::max(off, align_up(iv.second, kAlign));
+    }
+    bl.offset = off;
+    total = std::max(total, off + bl.bytes);
+    placed.push_back(i);
+  }
+  return align_up(total, kAlign);
+}
+
+enum Arena { AR_POOL = 0, AR_PERSIST = 1, AR_WORK = 2 };
+
+struct TensorLoc {
+  std::vector<int> labels;   // memory layout, row-major (last fastest)
+  int64_t size = 1;
+  int arena = AR_WORK;
+  int phase = 1;             // 0 hoist, 1 slice (work arena blocks)
+  int block = -1;
+  int64_t offset = 0;        // pool: element offset; persist: byte offset
+};
+
+enum VKind { VK_SIMT_T = 0, VK_SIMT_W = 1, VK_SIMT_S = 2, VK_GEMM = 3 };
+
+struct Vertex {
+  int ssa = 0, a = 0, b = 0;
+  bool dep = false, hoisted = false;
+  int kind = VK_SIMT_T;
+  u128 macs = 0;
+  std::vector<int> bl, cl, ml, nl, dxl, dyl;
+  int64_t B = 1, M = 1, N = 1, K = 1, kp = 0, sum_size = 1;
+  int nsplit = 0;
+  int64_t chunk = 0;
+  int blk_apl = -1, blk_bpl = -1, blk_part = -1;
+  int64_t tab_off = -1;  // element offset in the sum-table buffer
+};
+
+enum LaunchType { L_GATHER, L_SIMT, L_PACK, L_GEMM, L_ACCUM };
+struct Launch {
+  int type;
+  int idx;
+  int vertex;  // ssa id or -1
+};
+
+struct Plan {
+  int device = 0, precision = 1;
+  uint32_t flags = 0;
+  double gemm_min_macs = 0;
+  int L = 0, n = 0;
+  std::vector<int64_t> dims;
+  std::vector<std::vector<int>> leaf_labels;
+  std::vector<std::pair<int, int>> pairs;
+  std::vector<int> output, sliced;
+  std::vector<int> slice_pos;  // label -> position in sliced or -1
+  u128 d = 1;
+  std::vector<std::vector<std::pair<int, int>>> terms;
+  std::vector<int> parent;
+  std::vector<char> dep;
+  std::vector<TensorLoc> T;
+  std::vector<Vertex> V;  // index k <-> ssa n+k
+  std::vector<int> hoist_order, slice_order;
+  std::vector<int> gather_leaves;
+  std::vector<int64_t> pool_off;
+  int64_t pool_elems = 0;
+  std::vector<Block> blocks[2];
+  int64_t work_bytes = 0, persist_bytes = 0;
+  u128 ops = 0;
+  double width = 0;
+  u128 peak = 0;
+  int64_t out_size = 1;
+  bool too_wide = false;
+  std::vector<Int2Off> tables;
+  int64_t max_partial = 0;
+
+  // device state
+  bool bound = false;
+  float2* pool = nullptr;
+  char* work = nullptr;
+  char* persist = nullptr;
+  float2* partial = nullptr;
+  Int2Off* d_tabs = nullptr;
+  GatherJob* d_jobs = nullptr;
+  int njobs = 0;
+  double2* acc = nullptr;
+  double2* comp = nullptr;
+  unsigned long long* counter = nullptr;
+  cudaStream_t own = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  std::vector<Launch> hoist_launches, slice_launches;
+  std::vector<SimtParams> simt;
+  std::vector<PackParams> packs;
+  std::vector<GemmPlan> gemms;
+  AccumParams accum{};
+  std::vector<float2> staging;
+
+  ~Plan() { release(); }
+  void release() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (graph) cudaGraphDestroy(graph);
+    gexec = nullptr;
+    graph = nullptr;
+    void* ptrs[] = {pool, work, persist, partial, d_tabs, d_jobs, acc, comp, counter};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    pool = nullptr;
+    work = persist = nullptr;
+    partial = nullptr;
+    d_tabs = nullptr;
+    d_jobs = nullptr;
+    acc = comp = nullptr;
+    counter = nullptr;
+    if (own) cudaStreamDestroy(own);
+    own = nullptr;
+    bound = false;
+  }
+
+  int64_t prod(const std::vector<int>& ls) const {
+    int64_t p = 1;
+    for (int l : ls) p *= dims[l];
+    return p;
+  }
+  int64_t stride_in(const TensorLoc& t, int label) const {
+    int64_t s = 1;
+    for (int i = (int)t.labels.size() - 1; i >= 0; --i) {
+      if (t.labels[i] == label) return s;
+      s *= dims[t.labels[i]];
+    }
+    return 0;
+  }
+  float2* ptr(const TensorLoc& t) const {
+    if (t.arena == AR_POOL) return pool + t.offset;
+    if (t.arena == AR_PERSIST) return reinterpret_cast<float2*>(persist + t.offset);
+    return reinterpret_cast<float2*>(work + blocks[t.phase][t.block].offset);
+  }
+  char* block_ptr(int phase, int blk) const { return work + blocks[phase][blk].offset; }
+};
+
+// Build a fused IdxMap over `labels` (iteration order, last fastest) with the
+// strides of up to two tensors (stride 0 when a label is absent).
+bool build_map(const Plan& P, const std::vector<int>& labels, const TensorLoc* t0,
+               const TensorLoc* t1, IdxMap& m, std::string& err) {
+  std::vector<int64_t> dm, s0, s1;
+  for (int l : labels) {
+    int64_t d = P.dims[l];
+    int64_t a = t0 ? P.stride_in(*t0, l) : 0;
+    int64_t b = t1 ? P.stride_in(*t1, l) : 0;
+    if (d == 1) continue;
+    if (!dm.empty() && s0.back() == a * d && s1.back() == b * d) {
+      dm.back() *= d;
+      s0.back() = a;
+      s1.back() = b;
+      continue;
+    }
+    dm.push_back(d);
+    s0.push_back(a);
+    s1.push_back(b);
+  }
+  std::memset(&m, 0, sizeof(m));
+  if ((int)dm.size() > kMaxGroups) {
+    err = "index map needs " + std::to_string(dm.size()) + " groups (max " +
+          std::to_string(kMaxGroups) + ")";
+    return false;
+  }
+  m.n = (int)dm.size();
+  for (int i = 0; i < m.n; ++i) {
+    m.dim[i] = dm[i];
+    m.st0[i] = s0[i];
+    m.st1[i] = s1[i];
+    int lg = -1;
+    if ((dm[i] & (dm[i] - 1)) == 0) {
+      lg = 0;
+      while ((int64_t(1) << lg) < dm[i]) ++lg;
+    }
+    m.lg[i] = (int8_t)lg;
+  }
+  return true;
+}
+
+std::string u128_str(u128 v) {
+  if (v == 0) return "0";
+  std::string s;
+  while (v) {
+    s.push_back(char('0' + int(v % 10)));
+    v /= 10;
+  }
+  std::reverse(s.begin(), s.end());
+  return s;
+}
+
+int compile(Plan& P, const tnx_plan_desc* D) {
+  P.L = D->num_labels;
+  P.n = D->num_leaves;
+  P.device = D->device;
+  P.precision = D->precision;
+  P.flags = D->flags;
+  P.gemm_min_macs = D->gemm_min_macs > 0 ? D->gemm_min_macs : double(1 << 22);
+  if (P.L < 0 || P.n < 1) return fail(TNX_ERR_INVALID, "empty tree");
+  P.dims.assign(D->label_dims, D->label_dims + P.L);
+  for (int l = 0; l < P.L; ++l)
+    if (P.dims[l] < 1) return fail(TNX_ERR_DATA, "index " + std::to_string(l) + " has non-positive dim");
+  // leaves
+  int64_t pos = 0;
+  P.leaf_labels.resize(P.n);
+  std::vector<int> app(P.L, 0);
+  for (int i = 0; i < P.n; ++i) {
+    int r = D->leaf_ranks[i];
+    if (r < 0) return fail(TNX_ERR_DATA, "negative leaf rank");
+    std::vector<int>& ls = P.leaf_labels[i];
+    for (int j = 0; j < r; ++j) {
+      int l = D->leaf_labels[pos + j];
+      if (l < 0 || l >= P.L) return fail(TNX_ERR_DATA, "unknown index id in leaf " + std::to_string(i));
+      if (std::find(ls.begin(), ls.end(), l) != ls.end())
+        return fail(TNX_ERR_DATA, "repeated index in leaf " + std::to_string(i));
+      ls.push_back(l);
+      app[l] += 1;
+    }
+    pos += r;
+  }
+  for (int j = 0; j < D->num_output; ++j) {
+    int l = D->output_labels[j];
+    if (l < 0 || l >= P.L) return fail(TNX_ERR_DATA, "unknown output index");
+    if (app[l] == 0) return fail(TNX_ERR_DATA, "output index appears in no node");
+    if (std::find(P.output.begin(), P.output.end(), l) != P.output.end())
+      return fail(TNX_ERR_DATA, "repeated output index");
+    P.output.push_back(l);
+  }
+  for (int l : P.output) app[l] += 1;
+  P.slice_pos.assign(P.L, -1);
+  for (int j = 0; j < D->num_sliced; ++j) {
+    int l = D->sliced_labels[j];
+    if (l < 0 || l >= P.L) return fail(TNX_ERR_INVALID, "unknown sliced label");
+    if (P.slice_pos[l] >= 0) return fail(TNX_ERR_INVALID, "repeated label in slice set");
+    if (std::find(P.output.begin(), P.output.end(), l) != P.output.end())
+      return fail(TNX_ERR_INVALID, "output label cannot be sliced");
+    P.slice_pos[l] = (int)P.sliced.size();
+    P.sliced.push_back(l);
+    P.d *= (u128)P.dims[l];
+  }
+  if (P.d > (u128)(~0ull >> 1)) return fail(TNX_ERR_INVALID, "d_sliced exceeds 2^63");
+  // tree validation (tree.py:43-56)
+  const int nv = P.n > 1 ? 2 * P.n - 1 : 1;
+  P.pairs.resize(P.n - 1);
+  P.parent.assign(nv, -1);
+  for (int k = 0; k < P.n - 1; ++k) {
+    int a = D->pairs[2 * k], b = D->pairs[2 * k + 1];
+    for (int c : {a, b}) {
+      if (c < 0 || c >= P.n + k)
+        return fail(TNX_ERR_INVALID, "pair " + std::to_string(k) + " references unbuilt vertex " + std::to_string(c));
+      if (P.parent[c] >= 0) return fail(TNX_ERR_INVALID, "vertex " + std::to_string(c) + " consumed twice");
+      P.parent[c] = P.n + k;
+    }
+    if (a == b) return fail(TNX_ERR_INVALID, "vertex consumed twice");
+    P.pairs[k] = {a, b};
+  }
+  // terms (label-count saturation)
+  P.terms.resize(nv);
+  for (int i = 0; i < P.n; ++i)
+    for (int l : P.leaf_labels[i]) P.terms[i].push_back({l, 1});
+  std::vector<int> cnt(P.L, 0), seen(P.L, -1);
+  for (int k = 0; k < P.n - 1; ++k) {
+    const auto& ta = P.terms[P.pairs[k].first];
+    const auto& tb = P.terms[P.pairs[k].second];
+    auto& out = P.terms[P.n + k];
+    for (auto& e : tb) {
+      cnt[e.first] = e.second;
+      seen[e.first] = k;
+    }
+    for (auto& e : ta) {
+      int c = e.second + (seen[e.first] == k ? cnt[e.first] : 0);
+      if (c < app[e.first]) out.push_back({e.first, c});
+    }
+    for (auto& e : ta) seen[e.first] = -2 - k;  // mark as present in a
+    for (auto& e : tb) {
+      if (seen[e.first] == -2 - k) continue;
+      if (e.second < app[e.first]) out.push_back({e.first, e.second});
+    }
+  }
+  // dependence on sliced labels
+  P.dep.assign(nv, 0);
+  for (int i = 0; i < P.n; ++i)
+    for (int l : P.leaf_labels[i])
+      if (P.slice_pos[l] >= 0) P.dep[i] = 1;
+  for (int k = 0; k < P.n - 1; ++k)
+    P.dep[P.n + k] = P.dep[P.pairs[k].first] | P.dep[P.pairs[k].second];
+  const bool hoist = P.d > 1 && !(P.flags & TNX_FLAG_NO_HOIST);
+
+  // leaf pool + leaf tensors
+  P.T.resize(nv);
+  P.pool_off.resize(P.n);
+  int64_t poff = 0;
+  for (int i = 0; i < P.n; ++i) {
+    int64_t sz = 1;
+    for (int l : P.leaf_labels[i]) sz *= P.dims[l];
+    P.pool_off[i] = poff;
+    poff += align_up(sz, 32);
+  }
+  P.pool_elems = std::max<int64_t>(poff, 32);
+  for (int i = 0; i < P.n; ++i) {
+    TensorLoc& t = P.T[i];
+    bool sl = false;
+    for (int l : P.leaf_labels[i]) {
+      if (P.slice_pos[l] >= 0) sl = true;
+      else t.labels.push_back(l);
+    }
+    t.size = P.prod(t.labels);
+    if (!sl) {
+      t.arena = AR_POOL;
+      t.offset = P.pool_off[i];
+    } else {
+      t.arena = AR_WORK;
+      t.phase = 1;
+      P.gather_leaves.push_back(i);
+    }
+  }
+  // bookkeeping: ops, width
+  P.V.resize(P.n - 1);
+  P.peak = 0;
+  for (int k = 0; k < P.n - 1; ++k) {
+    Vertex& v = P.V[k];
+    v.ssa = P.n + k;
+    v.a = P.pairs[k].first;
+    v.b = P.pairs[k].second;
+    v.dep = P.dep[v.ssa];
+    v.hoisted = hoist && !v.dep;
+    u128 m = 1;
+    std::vector<char> mark(P.L, 0);
+    for (auto& e : P.terms[v.a]) mark[e.first] = 1;
+    for (auto& e : P.terms[v.b]) mark[e.first] = 1;
+    for (int l = 0; l < P.L; ++l)
+      if (mark[l] && P.slice_pos[l] < 0) m *= (u128)P.dims[l];
+    v.macs = m;
+    P.ops += m;
+    u128 sz = 1;
+    for (auto& e : P.terms[v.ssa])
+      if (P.slice_pos[e.first] < 0) sz *= (u128)P.dims[e.first];
+    P.peak = std::max(P.peak, sz);
+  }
+  for (int l : P.output) P.out_size *= P.dims[l];
+  if (P.n == 1) P.peak = (u128)P.out_size;
+  P.width = (double)std::log2((long double)P.peak);
+  // bookkeeping is exact at any width; lowering only for executable widths
+  if (P.peak >= ((u128)1 << 40)) {
+    P.too_wide = true;
+    return TNX_OK;
+  }
+
+  // execution order
+  for (int k = 0; k < P.n - 1; ++k) (P.V[k].hoisted ? P.hoist_order : P.slice_order).push_back(k);
+
+  // per-vertex lowering + memory blocks
+  auto add_block = [&](int phase, int64_t bytes, int first, int last) {
+    Block b;
+    b.bytes = align_up(std::max<int64_t>(bytes, 16), kAlign);
+    b.first = first;
+    b.last = last;
+    P.blocks[phase].push_back(b);
+    return (int)P.blocks[phase].size() - 1;
+  };
+  // step index of each vertex within its phase (slice phase: gather = 0)
+  std::vector<int> step(nv, 0);
+  for (size_t i = 0; i < P.hoist_order.size(); ++i) step[P.n + P.hoist_order[i]] = (int)i;
+  for (size_t i = 0; i < P.slice_order.size(); ++i) step[P.n + P.slice_order[i]] = (int)i + 1;
+  const int accum_step = (int)P.slice_order.size() + 1;
+  const int root = P.n > 1 ? 2 * P.n - 2 : 0;
+  auto consumer_step = [&](int v) {
+    int p = P.parent[v];
+    if (p < 0) return accum_step;  // root
+    return step[p];
+  };
+  for (int i : P.gather_leaves)
+    P.T[i].block = add_block(1, P.T[i].size * 8, 0, consumer_step(i));
+
+  int64_t persist_off = 0;
+  for (int k = 0; k < P.n - 1; ++k) {
+    Vertex& v = P.V[k];
+    const TensorLoc& x = P.T[v.a];
+    const TensorLoc& y = P.T[v.b];
+    std::vector<char> inx(P.L, 0), iny(P.L, 0), keep(P.L, 0);
+    for (int l : x.labels) inx[l] = 1;
+    for (int l : y.labels) iny[l] = 1;
+    for (auto& e : P.terms[v.ssa])
+      if (P.slice_pos[e.first] < 0) keep[e.first] = 1;
+    for (int l : x.labels) {
+      if (iny[l]) (keep[l] ? v.bl : v.cl).push_back(l);
+      else (keep[l] ? v.ml : v.dxl).push_back(l);
+    }
+    for (int l : y.labels)
+      if (!inx[l]) (keep[l] ? v.nl : v.dyl).push_back(l);
+    v.B = P.prod(v.bl);
+    v.M = P.prod(v.ml);
+    v.N = P.prod(v.nl);
+    v.K = P.prod(v.cl);
+    v.sum_size = v.K * P.prod(v.dxl) * P.prod(v.dyl);
+    TensorLoc& z = P.T[v.ssa];
+    const bool gemm = P.precision == TNX_PREC_3XTF32 && v.dxl.empty() && v.dyl.empty() &&
+                      v.M >= 128 && v.N >= 128 && v.K >= 16 &&
+                      (double)v.macs >= P.gemm_min_macs;
+    if (gemm) {
+      v.kind = VK_GEMM;
+      z.labels = v.bl;
+      z.labels.insert(z.labels.end(), v.ml.begin(), v.ml.end());
+      z.labels.insert(z.labels.end(), v.nl.begin(), v.nl.end());
+      v.kp = align_up(v.K, 16);
+    } else {
+      for (int l : x.labels)
+        if (keep[l]) z.labels.push_back(l);
+      for (int l : y.labels)
+        if (keep[l] && !inx[l]) z.labels.push_back(l);
+      const int64_t out = P.prod(z.labels);
+      const int64_t par = 148 * 2048;
+      if (v.sum_size <= 64 || out >= par / 2) v.kind = VK_SIMT_T;
+      else if (out * 32 >= par / 2) v.kind = VK_SIMT_W;
+      else {
+        v.kind = VK_SIMT_S;
+        int64_t ns = std::max<int64_t>(1, std::min<int64_t>((1184 + out - 1) / out, (v.sum_size + 2047) / 2048));
+        v.nsplit = (int)ns;
+        v.chunk = (v.sum_size + ns - 1) / ns;
+        P.max_partial = std::max(P.max_partial, out * ns);
+      }
+    }
+    z.size = P.prod(z.labels);
+    // placement of the result
+    const int ph = v.hoisted ? 0 : 1;
+    const int st = step[v.ssa];
+    const int par = P.parent[v.ssa];
+    if (v.hoisted && (par < 0 || !P.V[par - P.n].hoisted)) {
+      z.arena = AR_PERSIST;
+      z.offset = persist_off;
+      persist_off += align_up(z.size * 8, kAlign);
+    } else {
+      z.arena = AR_WORK;
+      z.phase = ph;
+      int last = v.hoisted ? (par >= 0 ? step[par] : st) : consumer_step(v.ssa);
+      z.block = add_block(ph, z.size * 8, st, last);
+    }
+    if (v.kind == VK_GEMM) {
+      v.blk_apl = add_block(ph, 16 * v.B * v.M * v.kp, st, st);
+      v.blk_bpl = add_block(ph, 16 * v.B * v.N * v.kp, st, st);
+    }
+  }
+  P.persist_bytes = std::max<int64_t>(persist_off, kAlign);
+  P.work_bytes = std::max(pack_blocks(P.blocks[0]), pack_blocks(P.blocks[1]));
+  P.work_bytes = std::max<int64_t>(P.work_bytes, kAlign);
+  (void)root;
+  return TNX_OK;
+}
+
+int run_launches(Plan& P, const std::vector<Launch>& ls, cudaStream_t st, int stop_vertex) {
+  for (const Launch& L : ls) {
+    cudaError_t e = cudaSuccess;
+    switch (L.type) {
+      case L_GATHER:
+        e = launch_gather(P.d_jobs, P.njobs, P.pool, P.counter, st);
+        break;
+      case L_SIMT:
+        e = launch_simt(P.simt[L.idx], st);
+        break;
+      case L_PACK:
+        e = launch_pack(P.packs[L.idx], st);
+        break;
+      case L_GEMM:
+        e = launch_gemm(P.gemms[L.idx], st);
+        break;
+      case L_ACCUM:
+        if (stop_vertex >= 0) continue;
+        e = launch_accum(P.accum, st);
+        break;
+    }
+    if (e != cudaSuccess) return fail(TNX_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+    if (stop_vertex >= 0 && L.vertex == stop_vertex && L.type != L_PACK) break;
+  }
+  return TNX_OK;
+}
+
+// Resolve pointers / tensor maps of every launch.  Requires arenas.
+int lower(Plan& P) {
+  std::string err;
+  char ebuf[256];
+  P.simt.clear();
+  P.packs.clear();
+  P.gemms.clear();
+  P.hoist_launches.clear();
+  P.slice_launches.clear();
+  if (!P.gather_leaves.empty()) P.slice_launches.push_back({L_GATHER, 0, -1});
+  for (int phase = 0; phase < 2; ++phase) {
+    const std::vector<int>& order = phase == 0 ? P.hoist_order : P.slice_order;
+    std::vector<Launch>& out = phase == 0 ? P.hoist_launches : P.slice_launches;
+    for (int k : order) {
+      Vertex& v = P.V[k];
+      const TensorLoc& x = P.T[v.a];
+      const TensorLoc& y = P.T[v.b];
+      const TensorLoc& z = P.T[v.ssa];
+      if (v.kind == VK_GEMM) {
+        float* apl = reinterpret_cast<float*>(P.block_ptr(phase, v.blk_apl));
+        float* bpl = reinterpret_cast<float*>(P.block_ptr(phase, v.blk_bpl));
+        PackParams pa{};
+        std::vector<int> rows_a = v.bl;
+        rows_a.insert(rows_a.end(), v.ml.begin(), v.ml.end());
+        if (!build_map(P, rows_a, &x, nullptr, pa.row, err) || !build_map(P, v.cl, &x, nullptr, pa.col, err))
+          return fail(TNX_ERR_INVALID, "vertex " + std::to_string(v.ssa) + ": " + err);
+        pa.src = P.ptr(x);
+        pa.dst = apl;
+        pa.rows = v.B * v.M;
+        pa.K = v.K;
+        pa.kp = v.kp;
+        pa.plane_stride = pa.rows * v.kp;
+        PackParams pb{};
+        std::vector<int> rows_b = v.bl;
+        rows_b.insert(rows_b.end(), v.nl.begin(), v.nl.end());
+        if (!build_map(P, rows_b, &y, nullptr, pb.row, err) || !build_map(P, v.cl, &y, nullptr, pb.col, err))
+          return fail(TNX_ERR_INVALID, "vertex " + std::to_string(v.ssa) + ": " + err);
+        pb.src = P.ptr(y);
+        pb.dst = bpl;
+        pb.rows = v.B * v.N;
+        pb.K = v.K;
+        pb.kp = v.kp;
+        pb.plane_stride = pb.rows * v.kp;
+        P.packs.push_back(pa);
+        out.push_back({L_PACK, (int)P.packs.size() - 1, v.ssa});
+        P.packs.push_back(pb);
+        out.push_back({L_PACK, (int)P.packs.size() - 1, v.ssa});
+        GemmPlan g;
+        if (gemm_prepare(&g, apl, bpl, P.ptr(z), v.B, v.M, v.N, v.kp, ebuf, sizeof(ebuf)))
+          return fail(TNX_ERR_CUDA, std::string("vertex ") + std::to_string(v.ssa) + ": " + ebuf);
+        P.gemms.push_back(g);
+        out.push_back({L_GEMM, (int)P.gemms.size() - 1, v.ssa});
+      } else {
+        SimtParams s{};
+        std::vector<int> sum = v.cl;
+        sum.insert(sum.end(), v.dxl.begin(), v.dxl.end());
+        sum.insert(sum.end(), v.dyl.begin(), v.dyl.end());
+        if (!build_map(P, z.labels, &x, &y, s.out, err) || !build_map(P, sum, &x, &y, s.sum, err))
+          return fail(TNX_ERR_INVALID, "vertex " + std::to_string(v.ssa) + ": " + err);
+        s.x = P.ptr(x);
+        s.y = P.ptr(y);
+        s.z = P.ptr(z);
+        s.out_size = z.size;
+        s.sum_size = v.sum_size;
+        s.mode = v.kind;
+        s.nsplit = v.nsplit;
+        s.chunk = v.chunk;
+        s.partial = P.partial;
+        s.sum_tab = v.tab_off >= 0 ? P.d_tabs + v.tab_off : nullptr;
+        P.simt.push_back(s);
+        out.push_back({L_SIMT, (int)P.simt.size() - 1, v.ssa});
+      }
+    }
+  }
+  // accumulate: root -> output order
+  const int root = P.n > 1 ? 2 * P.n - 2 : 0;
+  const TensorLoc& r = P.T[root];
+  std::vector<int> extra;
+  for (int l : r.labels)
+    if (std::find(P.output.begin(), P.output.end(), l) == P.output.end()) extra.push_back(l);
+  std::memset(&P.accum, 0, sizeof(P.accum));
+  if (!build_map(P, P.output, &r, nullptr, P.accum.out, err) || !build_map(P, extra, &r, nullptr, P.accum.extra, err))
+    return fail(TNX_ERR_INVALID, "accumulate: " + err);
+  P.accum.root = P.ptr(r);
+  P.accum.acc = P.acc;
+  P.accum.comp = P.comp;
+  P.accum.out_size = P.out_size;
+  P.accum.extra_size = P.prod(extra);
+  P.accum.slice_counter = P.counter;
+  P.slice_launches.push_back({L_ACCUM, 0, -1});
+  return TNX_OK;
+}
+
+// Precomputed summed-index offset tables (int32) for small SIMT sums.
+void build_tables(Plan& P) {
+  P.tables.clear();
+  for (auto& v : P.V) {
+    v.tab_off = -1;
+    if (v.kind == VK_GEMM || v.kind == VK_SIMT_S || v.sum_size > 4096) continue;
+    const TensorLoc& x = P.T[v.a];
+    const TensorLoc& y = P.T[v.b];
+    std::vector<int> sum = v.cl;
+    sum.insert(sum.end(), v.dxl.begin(), v.dxl.end());
+    sum.insert(sum.end(), v.dyl.begin(), v.dyl.end());
+    std::vector<int64_t> sx, sy, dm;
+    for (int l : sum) {
+      dm.push_back(P.dims[l]);
+      sx.push_back(P.stride_in(x, l));
+      sy.push_back(P.stride_in(y, l));
+    }
+    bool fits = x.size < (int64_t(1) << 31) && y.size < (int64_t(1) << 31);
+    if (!fits) continue;
+    v.tab_off = (int64_t)P.tables.size();
+    std::vector<int64_t> dig(dm.size(), 0);
+    for (int64_t j = 0; j < v.sum_size; ++j) {
+      int64_t ox = 0, oy = 0;
+      for (size_t i = 0; i < dm.size(); ++i) {
+        ox += dig[i] * sx[i];
+        oy += dig[i] * sy[i];
+      }
+      P.tables.push_back({(int32_t)ox, (int32_t)oy});
+      for (int i = (int)dm.size() - 1; i >= 0; --i) {
+        if (++dig[i] < dm[i]) break;
+        dig[i] = 0;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tnx_last_error(void) { return g_err.c_str(); }
+const char* tnx_version(void) { return "tnx 0.1 (sm_100a, tcgen05 split-TF32)"; }
+
+int tnx_plan_create(const tnx_plan_desc* desc, void** plan_out) {
+  if (!desc || !plan_out) return fail(TNX_ERR_INVALID, "null argument");
+  std::unique_ptr<Plan> P(new Plan());
+  int rc = compile(*P, desc);
+  if (rc) return rc;
+  if (!P->too_wide) build_tables(*P);
+  *plan_out = P.release();
+  return TNX_OK;
+}
+
+int tnx_plan_destroy(void* plan) {
+  if (!plan) return TNX_OK;
+  Plan* P = static_cast<Plan*>(plan);
+  if (P->bound) cudaSetDevice(P->device);
+  delete P;
+  return TNX_OK;
+}
+
+int tnx_bind_leaves(void* plan, const void* const* leaf_data, int32_t dtype, int32_t location,
+                    void* stream) {
+  if (!plan || !leaf_data) return fail(TNX_ERR_INVALID, "null argument");
+  Plan& P = *static_cast<Plan*>(plan);
+  if (P.too_wide)
+    return fail(TNX_ERR_OOM, "W_s=" + std::to_string(P.width) + " cannot be executed; slice more labels");
+  TNX_CUDA(cudaSetDevice(P.device));
+  if (!P.bound) {
+    char ebuf[256];
+    if (P.precision == TNX_PREC_3XTF32 && gemm_init_attributes(ebuf, sizeof(ebuf)))
+      return fail(TNX_ERR_CUDA, ebuf);
+    size_t free_b = 0, total_b = 0;
+    TNX_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const int64_t need = P.pool_elems * 8 + P.work_bytes + P.persist_bytes + P.max_partial * 8 +
+                         (int64_t)P.tables.size() * 8 + P.out_size * 32;
+    if ((double)need > 0.97 * (double)free_b)
+      return fail(TNX_ERR_OOM, "plan needs " + std::to_string(need) + " bytes of HBM, " +
+                                   std::to_string(free_b) + " free");
+    TNX_CUDA(cudaStreamCreateWithFlags(&P.own, cudaStreamNonBlocking));
+    TNX_CUDA(cudaMalloc(&P.pool, P.pool_elems * 8));
+    TNX_CUDA(cudaMalloc(&P.work, P.work_bytes));
+    TNX_CUDA(cudaMalloc(&P.persist, P.persist_bytes));
+    if (P.max_partial) TNX_CUDA(cudaMalloc(&P.partial, P.max_partial * 8));
+    if (!P.tables.empty()) {
+      TNX_CUDA(cudaMalloc(&P.d_tabs, P.tables.size() * sizeof(Int2Off)));
+      TNX_CUDA(cudaMemcpy(P.d_tabs, P.tables.data(), P.tables.size() * sizeof(Int2Off), cudaMemcpyHostToDevice));
+    }
+    TNX_CUDA(cudaMalloc(&P.acc, std::max<int64_t>(P.out_size, 1) * 16));
+    TNX_CUDA(cudaMalloc(&P.comp, std::max<int64_t>(P.out_size, 1) * 16));
+    TNX_CUDA(cudaMalloc(&P.counter, 8));
+    // gather jobs
+    std::vector<GatherJob> jobs;
+    for (int i : P.gather_leaves) {
+      GatherJob j{};
+      const std::vector<int>& ls = P.leaf_labels[i];
+      if ((int)ls.size() > kMaxLeafRank) return fail(TNX_ERR_INVALID, "leaf rank exceeds 16");
+      j.src = P.pool_off[i];
+      j.dst = reinterpret_cast<float2*>(P.block_ptr(1, P.T[i].block));
+      j.out_size = P.T[i].size;
+      int64_t s = 1;
+      std::vector<int64_t> st(ls.size());
+      for (int q = (int)ls.size() - 1; q >= 0; --q) {
+        st[q] = s;
+        s *= P.dims[ls[q]];
+      }
+      for (size_t q = 0; q < ls.size(); ++q) {
+        int l = ls[q];
+        if (P.slice_pos[l] >= 0) {
+          u128 rad = 1;
+          for (size_t t = P.slice_pos[l] + 1; t < P.sliced.size(); ++t) rad *= (u128)P.dims[P.sliced[t]];
+          j.radix[j.n_sl] = (uint64_t)rad;
+          j.sdim[j.n_sl] = P.dims[l];
+          j.sst[j.n_sl] = st[q];
+          j.n_sl++;
+        } else {
+          j.kdim[j.n_kept] = P.dims[l];
+          j.kst[j.n_kept] = st[q];
+          j.n_kept++;
+        }
+      }
+      jobs.push_back(j);
+    }
+    P.njobs = (int)jobs.size();
+    if (P.njobs) {
+      TNX_CUDA(cudaMalloc(&P.d_jobs, jobs.size() * sizeof(GatherJob)));
+      TNX_CUDA(cudaMemcpy(P.d_jobs, jobs.data(), jobs.size() * sizeof(GatherJob), cudaMemcpyHostToDevice));
+    }
+    int rc = lower(P);
+    if (rc) return rc;
+    P.bound = true;
+  }
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.own;
+  // upload leaves
+  int64_t max_leaf = 0;
+  for (int i = 0; i < P.n; ++i) max_leaf = std::max<int64_t>(max_leaf, P.prod(P.leaf_labels[i]));
+  if (location == TNX_LOC_HOST) {
+    if (dtype == TNX_DTYPE_C128) {
+      P.staging.assign(P.pool_elems, make_float2(0.f, 0.f));
+      for (int i = 0; i < P.n; ++i) {
+        const double* src = static_cast<const double*>(leaf_data[i]);
+        int64_t sz = P.prod(P.leaf_labels[i]);
+        for (int64_t e = 0; e < sz; ++e)
+          P.staging[P.pool_off[i] + e] = make_float2((float)src[2 * e], (float)src[2 * e + 1]);
+      }
+      TNX_CUDA(cudaMemcpyAsync(P.pool, P.staging.data(), P.pool_elems * 8, cudaMemcpyHostToDevice, st));
+    } else {
+      for (int i = 0; i < P.n; ++i)
+        TNX_CUDA(cudaMemcpyAsync(P.pool + P.pool_off[i], leaf_data[i], P.prod(P.leaf_labels[i]) * 8,
+                                 cudaMemcpyHostToDevice, st));
+    }
+  } else {
+    for (int i = 0; i < P.n; ++i) {
+      int64_t sz = P.prod(P.leaf_labels[i]);
+      if (dtype == TNX_DTYPE_C128) {
+        cudaError_t e = launch_convert_c128(static_cast<const double2*>(leaf_data[i]), P.pool + P.pool_off[i], sz, st);
+        if (e != cudaSuccess) return fail(TNX_ERR_CUDA, cudaGetErrorString(e));
+      } else {
+        TNX_CUDA(cudaMemcpyAsync(P.pool + P.pool_off[i], leaf_data[i], sz * 8, cudaMemcpyDeviceToDevice, st));
+      }
+    }
+  }
+  (void)max_leaf;
+  // hoisted (slice-invariant) subtrees, computed once
+  int rc = run_launches(P, P.hoist_launches, st, -1);
+  if (rc) return rc;
+  TNX_CUDA(cudaMemsetAsync(P.acc, 0, std::max<int64_t>(P.out_size, 1) * 16, st));
+  TNX_CUDA(cudaMemsetAsync(P.comp, 0, std::max<int64_t>(P.out_size, 1) * 16, st));
+  // per-slice graph
+  if (!(P.flags & TNX_FLAG_NO_GRAPH) && !P.gexec) {
+    cudaStream_t cs = P.own;
+    TNX_CUDA(cudaStreamSynchronize(st));
+    TNX_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    rc = run_launches(P, P.slice_launches, cs, -1);
+    cudaGraph_t g = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(cs, &g);
+    if (rc) return rc;
+    if (ce != cudaSuccess) return fail(TNX_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    P.graph = g;
+    TNX_CUDA(cudaGraphInstantiate(&P.gexec, g, 0));
+  }
+  return TNX_OK;
+}
+
+int tnx_run_slices(void* plan, uint64_t s_begin, uint64_t s_end, void* stream) {
+  if (!plan) return fail(TNX_ERR_INVALID, "null plan");
+  Plan& P = *static_cast<Plan*>(plan);
+  if (!P.bound) return fail(TNX_ERR_STATE, "tnx_run_slices before tnx_bind_leaves");
+  if ((u128)s_end > P.d || s_begin > s_end) return fail(TNX_ERR_INVALID, "slice range out of [0, d)");
+  TNX_CUDA(cudaSetDevice(P.device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.own;
+  if (s_begin == s_end) return TNX_OK;
+  cudaError_t e = launch_set_counter(P.counter, s_begin, st);
+  if (e != cudaSuccess) return fail(TNX_ERR_CUDA, cudaGetErrorString(e));
+  for (uint64_t s = s_begin; s < s_end; ++s) {
+    if (P.gexec) {
+      TNX_CUDA(cudaGraphLaunch(P.gexec, st));
+    } else {
+      int rc = run_launches(P, P.slice_launches, st, -1);
+      if (rc) return rc;
+    }
+  }
+  return TNX_OK;
+}
+
+int tnx_reset_accumulator(void* plan, void* stream) {
+  Plan& P = *static_cast<Plan*>(plan);
+  if (!P.bound) return fail(TNX_ERR_STATE, "not bound");
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.own;
+  TNX_CUDA(cudaMemsetAsync(P.acc, 0, std::max<int64_t>(P.out_size, 1) * 16, st));
+  TNX_CUDA(cudaMemsetAsync(P.comp, 0, std::max<int64_t>(P.out_size, 1) * 16, st));
+  return TNX_OK;
+}
+
+int tnx_partial_result(void* plan, double* out, int64_t out_elems, void* stream) {
+  Plan& P = *static_cast<Plan*>(plan);
+  if (!P.bound) return fail(TNX_ERR_STATE, "not bound");
+  if (out_elems != P.out_size) return fail(TNX_ERR_INVALID, "output size mismatch");
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.own;
+  TNX_CUDA(cudaMemcpyAsync(out, P.acc, P.out_size * 16, cudaMemcpyDeviceToHost, st));
+  TNX_CUDA(cudaStreamSynchronize(st));
+  return TNX_OK;
+}
+
+int tnx_stats_get(void* plan, tnx_stats* s) {
+  if (!plan || !s) return fail(TNX_ERR_INVALID, "null argument");
+  Plan& P = *static_cast<Plan*>(plan);
+  std::memset(s, 0, sizeof(*s));
+  s->op_count_lo = (uint64_t)P.ops;
+  s->op_count_hi = (uint64_t)(P.ops >> 64);
+  s->d_lo = (uint64_t)P.d;
+  s->d_hi = (uint64_t)(P.d >> 64);
+  s->width = P.width;
+  s->peak_elements = P.peak > (u128)~0ull ? ~0ull : (uint64_t)P.peak;
+  s->work_arena_bytes = P.work_bytes;
+  s->persistent_bytes = P.persist_bytes;
+  s->leaf_bytes = P.pool_elems * 8;
+  s->num_vertices = P.n - 1;
+  s->num_hoisted = (int)P.hoist_order.size();
+  int ng = 0, ns = 0, launches = P.gather_leaves.empty() ? 1 : 2;
+  for (int k : P.slice_order) {
+    if (P.V[k].kind == VK_GEMM) {
+      ++ng;
+      launches += 3;
+    } else {
+      ++ns;
+      launches += P.V[k].kind == VK_SIMT_S ? 2 : 1;
+    }
+  }
+  s->num_gemm = ng;
+  s->num_simt = ns;
+  s->launches_per_slice = launches;
+  s->out_rank = (int)P.output.size();
+  s->out_elements = P.out_size;
+  return TNX_OK;
+}
+
+int tnx_vertex_info_get(void* plan, int32_t index, tnx_vertex_info* out) {
+  Plan& P = *static_cast<Plan*>(plan);
+  if (index < 0 || index >= (int)P.V.size()) return fail(TNX_ERR_INVALID, "vertex index out of range");
+  const Vertex& v = P.V[index];
+  out->ssa = v.ssa;
+  out->kind = v.kind;
+  out->hoisted = v.hoisted;
+  out->rank = (int)P.T[v.ssa].labels.size();
+  out->m = v.M;
+  out->n = v.N;
+  out->k = v.K;
+  out->batch = v.B;
+  out->macs_lo = (uint64_t)v.macs;
+  out->macs_hi = (uint64_t)(v.macs >> 64);
+  return TNX_OK;
+}
+
+int tnx_debug_vertex(void* plan, uint64_t s, int32_t v, float* out_c64, int64_t out_elems,
+                     int32_t* layout_labels, int32_t* rank_out) {
+  Plan& P = *static_cast<Plan*>(plan);
+  if (!P.bound) return fail(TNX_ERR_STATE, "not bound");
+  const int nv = P.n > 1 ? 2 * P.n - 1 : 1;
+  if (v < P.n || v >= nv) return fail(TNX_ERR_INVALID, "vertex must be internal");
+  if ((u128)s >= P.d) return fail(TNX_ERR_INVALID, "slice out of range");
+  const TensorLoc& t = P.T[v];
+  if (out_elems != t.size) return fail(TNX_ERR_INVALID, "size mismatch: need " + std::to_string(t.size));
+  TNX_CUDA(cudaSetDevice(P.device));
+  cudaStream_t st = P.own;
+  TNX_CUDA(cudaStreamSynchronize(st));
+  const Vertex& vx = P.V[v - P.n];
+  int rc;
+  if (vx.hoisted) {
+    rc = run_launches(P, P.hoist_launches, st, v);
+  } else {
+    cudaError_t e = launch_set_counter(P.counter, s, st);
+    if (e != cudaSuccess) return fail(TNX_ERR_CUDA, cudaGetErrorString(e));
+    rc = run_launches(P, P.slice_launches, st, v);
+  }
+  if (rc) return rc;
+  TNX_CUDA(cudaMemcpyAsync(out_c64, P.ptr(t), t.size * 8, cudaMemcpyDeviceToHost, st));
+  TNX_CUDA(cudaStreamSynchronize(st));
+  for (size_t i = 0; i < t.labels.size(); ++i) layout_labels[i] = t.labels[i];
+  *rank_out = (int)t.labels.size();
+  return TNX_OK;
+}
+
+int tnx_synchronize(void* plan) {
+  Plan& P = *static_cast<Plan*>(plan);
+  TNX_CUDA(cudaSetDevice(P.device));
+  TNX_CUDA(cudaDeviceSynchronize());
+  return TNX_OK;
+}
+
+int tnx_gemm_c64(const void* A, const void* B, void* C, int64_t batch, int64_t M, int64_t N,
+                 int64_t K, int32_t precision, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char ebuf[256];
+  if (gemm_init_attributes(ebuf, sizeof(ebuf))) return fail(TNX_ERR_CUDA, ebuf);
+  const int64_t kp = align_up(K, 16);
+  float *apl = nullptr, *bpl = nullptr;
+  TNX_CUDA(cudaMalloc(&apl, 16 * batch * M * kp));
+  TNX_CUDA(cudaMalloc(&bpl, 16 * batch * N * kp));
+  auto simple = [&](IdxMap& m, int64_t rows, int64_t stride) {
+    std::memset(&m, 0, sizeof(m));
+    m.n = 1;
+    m.dim[0] = rows;
+    m.st0[0] = stride;
+    m.lg[0] = -1;
+  };
+  PackParams pa{}, pb{};
+  simple(pa.row, batch * M, K);
+  simple(pa.col, K, 1);
+  pa.src = static_cast<const float2*>(A);
+  pa.dst = apl;
+  pa.rows = batch * M;
+  pa.K = K;
+  pa.kp = kp;
+  pa.plane_stride = pa.rows * kp;
+  simple(pb.row, batch * N, K);
+  simple(pb.col, K, 1);
+  pb.src = static_cast<const float2*>(B);
+  pb.dst = bpl;
+  pb.rows = batch * N;
+  pb.K = K;
+  pb.kp = kp;
+  pb.plane_stride = pb.rows * kp;
+  cudaError_t e = launch_pack(pa, st);
+  if (e == cudaSuccess) e = launch_pack(pb, st);
+  if (e != cudaSuccess) return fail(TNX_ERR_CUDA, cudaGetErrorString(e));
+  (void)precision;
+  GemmPlan g;
+  if (gemm_prepare(&g, apl, bpl, static_cast<float2*>(C), batch, M, N, kp, ebuf, sizeof(ebuf)))
+    return fail(TNX_ERR_CUDA, ebuf);
+  e = launch_gemm(g, st);
+  if (e != cudaSuccess) return fail(TNX_ERR_CUDA, cudaGetErrorString(e));
+  TNX_CUDA(cudaStreamSynchronize(st));
+  cudaFree(apl);
+  cudaFree(bpl);
+  return TNX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,105 @@
+// Internal interface between the plan/runtime (tnx_api.cpp) and the CUDA
+// kernels (kernels.cu, gemm_tc.cu).  Plain structs passed by value as kernel
+// parameters; all offsets are in elements.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tnx {
+
+constexpr int kMaxGroups = 32;   // fused label groups per index map
+
+// Mixed-radix index map: linear index (row-major over the groups, last
+// fastest) -> two operand offsets.  lg[i] >= 0 marks a power-of-two extent.
+struct IdxMap {
+  int32_t n;
+  int32_t pad;
+  int64_t dim[kMaxGroups];
+  int64_t st0[kMaxGroups];
+  int64_t st1[kMaxGroups];
+  int8_t lg[kMaxGroups];
+};
+
+struct Int2Off { int32_t x, y; };
+
+enum SimtMode : int32_t { SIMT_THREAD = 0, SIMT_WARP = 1, SIMT_SPLIT = 2 };
+
+struct SimtParams {
+  IdxMap out;             // output index -> (x offset, y offset)
+  IdxMap sum;             // summed index -> (x offset, y offset)
+  const float2* x;
+  const float2* y;
+  float2* z;
+  float2* partial;        // SPLIT: [out_size][nsplit]
+  const Int2Off* sum_tab; // optional precomputed sum offsets (int32)
+  int64_t out_size;
+  int64_t sum_size;
+  int64_t chunk;          // SPLIT: sum elements per block
+  int32_t nsplit;
+  int32_t mode;
+};
+
+// Pack a complex64 tensor into four fp32 planes [re_hi, re_lo, im_hi, im_lo],
+// each [rows][kp] (rows = batch*R, K padded to kp with zeros); hi = tf32
+// truncation, lo = x - hi.
+struct PackParams {
+  IdxMap row;             // row index -> src offset (st0)
+  IdxMap col;             // k index (k < K) -> src offset (st0)
+  const float2* src;
+  float* dst;
+  int64_t rows;
+  int64_t K;
+  int64_t kp;
+  int64_t plane_stride;   // rows * kp
+};
+
+constexpr int kMaxLeafRank = 16;
+struct GatherJob {
+  int64_t src;            // element offset in the leaf pool
+  float2* dst;
+  int64_t out_size;
+  int32_t n_kept;
+  int32_t n_sl;
+  int64_t kdim[kMaxLeafRank];
+  int64_t kst[kMaxLeafRank];
+  uint64_t radix[kMaxLeafRank];   // suffix product of the slice dims
+  int64_t sdim[kMaxLeafRank];
+  int64_t sst[kMaxLeafRank];
+};
+
+struct AccumParams {
+  IdxMap out;             // output index -> root offset (st0)
+  IdxMap extra;           // extra summed labels (single-leaf tree) -> root offset
+  const float2* root;
+  double2* acc;
+  double2* comp;
+  int64_t out_size;
+  int64_t extra_size;
+  unsigned long long* slice_counter;  // advanced by one after the slice
+};
+
+// launchers (return cudaError_t)
+cudaError_t launch_gather(const GatherJob* jobs, int njobs, const float2* leaf_pool,
+                          const unsigned long long* slice_counter, cudaStream_t st);
+cudaError_t launch_simt(const SimtParams& p, cudaStream_t st);
+cudaError_t launch_pack(const PackParams& p, cudaStream_t st);
+cudaError_t launch_accum(const AccumParams& p, cudaStream_t st);
+cudaError_t launch_set_counter(unsigned long long* counter, unsigned long long v, cudaStream_t st);
+cudaError_t launch_convert_c128(const double2* src, float2* dst, int64_t n, cudaStream_t st);
+cudaError_t launch_zero(void* p, int64_t bytes, cudaStream_t st);
+
+// tcgen05 split-TF32 complex GEMM over packed planes.
+struct GemmPlan {
+  alignas(64) unsigned char tmap_a[128];   // CUtensorMap
+  alignas(64) unsigned char tmap_b[128];
+  float2* out;
+  int64_t M, N, kp, batch;
+  int32_t ok;
+};
+// Build tensor maps for planes laid out as [4][batch][M|N][kp] fp32.
+int gemm_prepare(GemmPlan* g, const float* a_planes, const float* b_planes, float2* out,
+                 int64_t batch, int64_t M, int64_t N, int64_t kp, char* err, size_t errlen);
+cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st);
+int gemm_init_attributes(char* err, size_t errlen);
+
+}  // namespace tnx

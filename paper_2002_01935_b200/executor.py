@@ -1,0 +1,389 @@
+"""B200 executor: the drop-in for the reference's SPEC executor entry points.
+
+* ``contract(tn, tree, options)`` -> (value-or-open-tensor, exponent10, op_count)
+  (`/root/reference/SPEC.md:515-523`)
+* ``contract_sliced(tn, tree, slice_set, options)`` -> same triple, summed over
+  every slice assignment; ``slice_ids`` restricts the sum
+  to a contiguous prefix/range (the paper's "first 100 slices" protocol,
+  PAPER.md:758).
+* ``amplitude(circuit_tn, bitstring, tree, ...)``: open
+  output legs projected onto the bitstring (column projection) -- the same
+  compiled plan is reused across bitstrings, only leaf data is re-bound.
+
+Everything numeric runs in libtnx.so on the GPU (hand-written sm_100a CUDA);
+this module only interns labels, owns the plan handle and converts results.
+Errors mirror the reference: ``ValueError`` for tree/slice problems,
+``DataError`` for network data problems, ``FloatingPointError`` for
+non-finite results.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import threading
+
+import numpy as np
+
+from . import _native as nat
+from .network import DataError, TensorNetwork, TensorNode
+
+__all__ = ["SlicedPlan", "contract", "contract_sliced", "amplitude", "AmplitudeEngine",
+           "PRECISIONS"]
+
+PRECISIONS = {"fp32": nat.PREC_FP32, "3xtf32": nat.PREC_3XTF32}
+
+
+def _as_labels(slice_set):
+    if slice_set is None:
+        return ()
+    if hasattr(slice_set, "labels"):
+        return tuple(slice_set.labels)
+    return tuple(slice_set)
+
+
+def _i32(values):
+    arr = (C.c_int32 * max(1, len(values)))(*values)
+    return arr
+
+
+class SlicedPlan:
+    """A compiled (network, tree, slice set) on one CUDA device.
+
+    Compilation (bookkeeping, kernel selection, HBM arena plan) happens in
+    libtnx at construction; ``bind`` uploads leaf data, precomputes the
+    slice-invariant subtrees and captures the per-slice CUDA graph; ``run``
+    contracts a slice range into the device accumulator.
+    """
+
+    def __init__(self, tn, tree, slice_set=(), device=0, precision="3xtf32", graph=True,
+                 hoist=True, gemm_min_macs=0.0):
+        lib = nat.load()
+        self.tn = tn
+        self.tree = tree
+        self.device = int(device)
+        self.sliced = _as_labels(slice_set)
+        if sorted(tree.leaves) != sorted(tn.node_ids):
+            raise ValueError("tree leaves do not match network node ids")
+        labels = list(tn.index_table)
+        self.labels = labels
+        lid = {l: i for i, l in enumerate(labels)}
+        self.label_ids = lid
+        for lbl in self.sliced:
+            if lbl not in lid:
+                raise ValueError(f"unknown sliced label {lbl}")
+        ranks, leaf_labels = [], []
+        for nid in tree.leaves:
+            nd = tn.node(nid)
+            for lbl in nd.indices:
+                if lbl not in lid:
+                    raise DataError(f"unknown index {lbl}@node{nd.id}")
+            ranks.append(len(nd.indices))
+            leaf_labels.extend(lid[l] for l in nd.indices)
+        pairs = [c for p in tree.pairs for c in p]
+        for lbl in tn.output:
+            if lbl not in lid:
+                raise DataError(f"unknown output index {lbl}")
+        self._keep = dict(
+            dims=(C.c_int64 * max(1, len(labels)))(*[tn.index_table[l] for l in labels]),
+            ranks=_i32(ranks), leaf_labels=_i32(leaf_labels), pairs=_i32(pairs),
+            out=_i32([lid[l] for l in tn.output]), sl=_i32([lid[l] for l in self.sliced]))
+        k = self._keep
+        flags = (0 if graph else nat.FLAG_NO_GRAPH) | (0 if hoist else nat.FLAG_NO_HOIST)
+        if precision not in PRECISIONS:
+            raise ValueError(f"unknown precision {precision!r}; choose from {sorted(PRECISIONS)}")
+        self.precision = precision
+        desc = nat.PlanDesc(len(labels), k["dims"], tree.n, k["ranks"], k["leaf_labels"], k["pairs"],
+                            len(tn.output), k["out"], len(self.sliced), k["sl"],
+                            PRECISIONS[precision], self.device, flags, 0, float(gemm_min_macs))
+        handle = C.c_void_p()
+        nat.check(lib.tnx_plan_create(C.byref(desc), C.byref(handle)))
+        self._h = handle
+        self._lib = lib
+        self._bound = False
+        st = nat.Stats()
+        nat.check(lib.tnx_stats_get(self._h, C.byref(st)))
+        self._stats = st
+        self.out_shape = tuple(tn.index_table[l] for l in tn.output)
+
+    # ------------------------------------------------------------ properties
+    @property
+    def d(self):
+        return self._stats.d_lo | (self._stats.d_hi << 64)
+
+    @property
+    def ops_per_slice(self):
+        """Exact per-slice MAC count sum_v U_v (C_s / d)."""
+        return self._stats.op_count_lo | (self._stats.op_count_hi << 64)
+
+    @property
+    def flops_per_slice(self):
+        return 8 * self.ops_per_slice
+
+    @property
+    def width(self):
+        return self._stats.width
+
+    def stats(self):
+        s = self._stats
+        return {"op_count_per_slice": self.ops_per_slice, "d": self.d, "W_s": s.width,
+                "peak_elements": s.peak_elements, "work_arena_bytes": s.work_arena_bytes,
+                "persistent_bytes": s.persistent_bytes, "leaf_bytes": s.leaf_bytes,
+                "num_vertices": s.num_vertices, "num_hoisted": s.num_hoisted,
+                "num_gemm": s.num_gemm, "num_simt": s.num_simt,
+                "launches_per_slice": s.launches_per_slice, "out_elements": s.out_elements}
+
+    def vertex_info(self):
+        out = []
+        vi = nat.VertexInfo()
+        for i in range(self._stats.num_vertices):
+            nat.check(self._lib.tnx_vertex_info_get(self._h, i, C.byref(vi)))
+            out.append({"ssa": vi.ssa, "kind": nat.KIND_NAMES[vi.kind], "hoisted": bool(vi.hoisted),
+                        "rank": vi.rank, "m": vi.m, "n": vi.n, "k": vi.k, "batch": vi.batch,
+                        "macs": vi.macs_lo | (vi.macs_hi << 64)})
+        return out
+
+    # ------------------------------------------------------------ execution
+    def bind(self, tn=None, stream=None, leaf_arrays=None):
+        """Upload leaf data (host complex128 from ``tn`` nodes, or a list of
+        contiguous complex64/complex128 host arrays / CUDA torch tensors in
+        SSA leaf order)."""
+        tn = self.tn if tn is None else tn
+        if leaf_arrays is None:
+            arrs = []
+            for nid in self.tree.leaves:
+                nd = tn.node(nid)
+                if nd.data is None:
+                    raise ValueError(f"contract needs dense data on every node (node {nid})")
+                arrs.append(np.ascontiguousarray(nd.data, dtype=np.complex128))
+            leaf_arrays = arrs
+        loc, dtype, ptrs, hold = self._leaf_pointers(leaf_arrays)
+        self._hold = hold
+        nat.check(self._lib.tnx_bind_leaves(self._h, ptrs, dtype, loc, self._stream(stream)))
+        self._bound = True
+        return self
+
+    def _leaf_pointers(self, arrays):
+        ptrs = (C.c_void_p * max(1, len(arrays)))()
+        first = arrays[0]
+        if hasattr(first, "is_cuda") and first.is_cuda:
+            import torch
+            dt = first.dtype
+            dtype = nat.DTYPE_C64 if dt == torch.complex64 else nat.DTYPE_C128
+            for i, a in enumerate(arrays):
+                ptrs[i] = a.contiguous().data_ptr()
+            return nat.LOC_DEVICE, dtype, ptrs, arrays
+        conv = []
+        dtype = nat.DTYPE_C64 if np.asarray(first).dtype == np.complex64 else nat.DTYPE_C128
+        want = np.complex64 if dtype == nat.DTYPE_C64 else np.complex128
+        for i, a in enumerate(arrays):
+            a = np.ascontiguousarray(a, dtype=want)
+            conv.append(a)
+            ptrs[i] = a.ctypes.data
+        return nat.LOC_HOST, dtype, ptrs, conv
+
+    @staticmethod
+    def _stream(stream):
+        if stream is None:
+            return None
+        if isinstance(stream, int):
+            return C.c_void_p(stream)
+        return C.c_void_p(stream.cuda_stream)
+
+    def run(self, s_begin=0, s_end=None, stream=None):
+        if not self._bound:
+            raise ValueError("bind() leaf data before run()")
+        s_end = self.d if s_end is None else s_end
+        nat.check(self._lib.tnx_run_slices(self._h, int(s_begin), int(s_end), self._stream(stream)))
+        return self
+
+    def reset(self, stream=None):
+        nat.check(self._lib.tnx_reset_accumulator(self._h, self._stream(stream)))
+
+    def result(self, stream=None):
+        n = int(self._stats.out_elements)
+        buf = np.zeros(2 * max(n, 1), dtype=np.float64)
+        nat.check(self._lib.tnx_partial_result(self._h, buf.ctypes.data_as(C.POINTER(C.c_double)), n,
+                                               self._stream(stream)))
+        val = (buf[0::2] + 1j * buf[1::2])[:n].reshape(self.out_shape)
+        return val
+
+    def synchronize(self):
+        nat.check(self._lib.tnx_synchronize(self._h))
+
+    def debug_vertex(self, s, v):
+        """Intermediate tensor of SSA vertex v for slice s: (labels, array)."""
+        info = [x for x in self.vertex_info() if x["ssa"] == v]
+        if not info:
+            raise ValueError("vertex must be internal")
+        rank = info[0]["rank"]
+        # size from layout: query with a probe buffer
+        lay = (C.c_int32 * max(1, rank))()
+        rk = C.c_int32()
+        size = self._vertex_size(v)
+        buf = np.zeros(2 * size, dtype=np.float32)
+        nat.check(self._lib.tnx_debug_vertex(self._h, int(s), int(v),
+                                             buf.ctypes.data_as(C.POINTER(C.c_float)), size, lay,
+                                             C.byref(rk)))
+        labels = tuple(self.labels[lay[i]] for i in range(rk.value))
+        shape = tuple(self.tn.index_table[l] for l in labels)
+        return labels, (buf[0::2] + 1j * buf[1::2]).astype(np.complex64).reshape(shape)
+
+    def _vertex_size(self, v):
+        from .tree import annotate_incidence
+        annotate_incidence(self.tree, self.tn)
+        size = 1
+        S = set(self.sliced)
+        for lbl in self.tree._ann.ordered_labels(v):
+            if lbl not in S:
+                size *= self.tn.index_table[lbl]
+        return size
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.tnx_plan_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def _finish(val, tn, strip_exponent):
+    arr = np.asarray(val)
+    if not np.all(np.isfinite(arr)):
+        raise FloatingPointError("non-finite contraction value")
+    exp10 = tn.norm_exponent
+    if strip_exponent:
+        m = float(np.max(np.abs(arr))) if arr.size else 0.0
+        if m > 0.0:
+            e = math.floor(math.log10(m))
+            arr = arr / 10.0 ** e
+            exp10 += e
+    if arr.ndim == 0:
+        return complex(arr), exp10
+    return arr, exp10
+
+
+def _slice_range(d, slice_ids):
+    if slice_ids is None:
+        return 0, d
+    if isinstance(slice_ids, range):
+        if slice_ids.step != 1:
+            raise ValueError("slice_ids must be a contiguous range")
+        return slice_ids.start, slice_ids.stop
+    s0, s1 = slice_ids
+    return int(s0), int(s1)
+
+
+def contract_sliced(tn, tree, slice_set=(), options=None, *, slice_ids=None, devices=(0,),
+                    precision="3xtf32", graph=True, hoist=True):
+    """Sum over slice assignments of the per-slice contraction.
+
+    Returns (value-or-open-tensor, exponent10, op_count) with op_count the
+    exact MAC count executed (C_s for the full range).  ``devices`` splits
+    the slice range into contiguous per-device blocks (one host thread per
+    device) and sums the complex128 partials.
+    """
+    options = dict(options or {})
+    strip = bool(options.get("strip_exponent", False))
+    devices = list(devices)
+    plans = [SlicedPlan(tn, tree, slice_set, device=d, precision=precision, graph=graph, hoist=hoist)
+             for d in devices]
+    try:
+        s0, s1 = _slice_range(plans[0].d, slice_ids)
+        if not 0 <= s0 <= s1 <= plans[0].d:
+            raise ValueError("slice range out of [0, d)")
+        G = len(plans)
+        bounds = [s0 + (s1 - s0) * g // G for g in range(G + 1)]
+        errs = [None] * G
+        parts = [None] * G
+
+        def work(g):
+            try:
+                p = plans[g]
+                p.bind()
+                p.run(bounds[g], bounds[g + 1])
+                parts[g] = p.result()
+            except BaseException as exc:  # noqa: BLE001
+                errs[g] = exc
+
+        if G == 1:
+            work(0)
+        else:
+            th = [threading.Thread(target=work, args=(g,)) for g in range(G)]
+            for t in th:
+                t.start()
+            for t in th:
+                t.join()
+        for e in errs:
+            if e is not None:
+                raise e
+        total = parts[0]
+        for p in parts[1:]:
+            total = total + p
+        ops = plans[0].ops_per_slice * (s1 - s0)
+        val, exp10 = _finish(total, tn, strip)
+        return val, exp10, ops
+    finally:
+        for p in plans:
+            p.close()
+
+
+def contract(tn, tree, options=None, **kw):
+    """Unsliced contraction."""
+    return contract_sliced(tn, tree, (), options, **kw)
+
+
+def _project(tn, bitstring):
+    """Fix the open legs (tn.output order) to the bitstring (column projection)."""
+    if len(bitstring) != len(tn.output):
+        raise ValueError(f"bitstring length {len(bitstring)} != {len(tn.output)} open legs")
+    fix = {lbl: int(b) for lbl, b in zip(tn.output, bitstring)}
+    nodes = []
+    for nd in tn.nodes:
+        data, labels = nd.data, list(nd.indices)
+        if data is None:
+            raise ValueError("amplitude needs dense data")
+        for lbl in list(labels):
+            if lbl in fix:
+                ax = labels.index(lbl)
+                if not 0 <= fix[lbl] < data.shape[ax]:
+                    raise ValueError(f"bit {fix[lbl]} out of range for leg {lbl}")
+                data = np.take(data, fix[lbl], axis=ax)
+                labels.pop(ax)
+        nodes.append(TensorNode(nd.id, labels, data))
+    table = {l: d for l, d in tn.index_table.items() if l not in fix}
+    return TensorNetwork(nodes, table, (), tn.norm_exponent)
+
+
+class AmplitudeEngine:
+    """One compiled plan reused across bitstrings (only leaf data changes,
+    PAPER.md:530)."""
+
+    def __init__(self, circuit_tn, tree, slice_set=(), device=0, precision="3xtf32"):
+        self.tn = circuit_tn
+        self.tree = tree
+        base = _project(circuit_tn, "0" * len(circuit_tn.output))
+        self.plan = SlicedPlan(base, tree, slice_set, device=device, precision=precision)
+
+    def __call__(self, bitstring):
+        ptn = _project(self.tn, bitstring)
+        self.plan.bind(ptn)
+        self.plan.run()
+        val, _ = _finish(self.plan.result(), ptn, False)
+        return val
+
+    def close(self):
+        self.plan.close()
+
+
+def amplitude(circuit_tn, bitstring, tree, slice_set=(), **kw):
+    """c_x = <x| U |0> of a circuit network whose open legs are the qubits."""
+    eng = AmplitudeEngine(circuit_tn, tree, slice_set, **kw)
+    try:
+        return eng(bitstring)
+    finally:
+        eng.close()

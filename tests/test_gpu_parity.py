@@ -1,0 +1,164 @@
+"""GPU parity: the B200 executor (through the C ABI) vs the CPU oracle and the
+reference golden vectors.  Tolerance: complex64 execution vs complex128
+reference, norm-wise relative error <= 1e-5 (north_star), with an absolute
+floor of 1e-5 * (value of the |.|-network) for cancelling random cases."""
+import numpy as np
+import pytest
+
+import oracle
+from conftest import arr_from_json, golden_cases
+from _util import case_objects, rel_err
+from paper_2002_01935_b200.executor import (SlicedPlan, contract, contract_sliced, amplitude,
+                                            AmplitudeEngine)
+from paper_2002_01935_b200.network import TensorNetwork, TensorNode
+from paper_2002_01935_b200.harness import generators as gen
+from paper_2002_01935_b200.harness.paths import best_greedy_tree, greedy_tree
+from paper_2002_01935_b200.slicing import greedy_slice, SliceSet
+from paper_2002_01935_b200.tree import metrics
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+def abs_network(tn):
+    return tn.replace(nodes=[TensorNode(nd.id, nd.indices, np.abs(nd.data)) for nd in tn.nodes])
+
+
+def check_close(got, ref, tn=None, tree=None, S=()):
+    got = np.asarray(got, dtype=np.complex128)
+    ref = np.asarray(ref, dtype=np.complex128)
+    err = np.linalg.norm((got - ref).ravel())
+    scale = np.linalg.norm(ref.ravel())
+    if tn is not None:
+        absval, _, _ = oracle.contract_sliced(abs_network(tn), tree, S)
+        scale = max(scale, 1e-2 * np.linalg.norm(np.asarray(absval).ravel()))
+    assert err <= TOL * scale, (err, scale)
+
+
+CASES = golden_cases()
+
+
+@pytest.mark.parametrize("precision", ["fp32", "3xtf32"])
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_golden_values(case, precision):
+    tn, tree = case_objects(case)
+    for ent in case["sliced"]:
+        if "value" not in ent:
+            continue
+        S = tuple(ent["labels"])
+        val, e10, ops = contract_sliced(tn, tree, S, precision=precision)
+        assert ops == int(ent["Cs"])
+        check_close(val, arr_from_json(ent["value"]), tn, tree, S)
+        for sid, v in ent.get("per_slice", {}).items():
+            got, _, _ = contract_sliced(tn, tree, S, slice_ids=(int(sid), int(sid) + 1),
+                                        precision=precision)
+            check_close(got, arr_from_json(v), tn, tree, S)
+
+
+def test_gemm_kernel_vs_numpy():
+    import torch
+    rng = np.random.default_rng(0)
+    from paper_2002_01935_b200 import _native as nat
+    lib = nat.load()
+    for (b, m, n, k) in [(1, 128, 128, 16), (1, 256, 384, 64), (2, 200, 136, 40), (1, 1024, 512, 1000),
+                         (3, 128, 256, 8)]:
+        A = (rng.standard_normal((b, m, k)) + 1j * rng.standard_normal((b, m, k))).astype(np.complex64)
+        B = (rng.standard_normal((b, n, k)) + 1j * rng.standard_normal((b, n, k))).astype(np.complex64)
+        ta = torch.from_numpy(A).cuda()
+        tb = torch.from_numpy(B).cuda()
+        tc = torch.zeros((b, m, n), dtype=torch.complex64, device="cuda")
+        nat.check(lib.tnx_gemm_c64(ta.data_ptr(), tb.data_ptr(), tc.data_ptr(), b, m, n, k, 1,
+                                   torch.cuda.current_stream().cuda_stream))
+        ref = np.einsum("bmk,bnk->bmn", A.astype(np.complex128), B.astype(np.complex128))
+        got = tc.cpu().numpy()
+        assert rel_err(got, ref) < 2e-6, (b, m, n, k, rel_err(got, ref))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_hyper_networks(seed):
+    tn = gen.random_hyper_network(8, 14, seed=100 + seed, max_rank=5)
+    tree = greedy_tree(tn, seed=seed)
+    ref, _, ops_ref = oracle.contract(tn, tree)
+    val, _, ops = contract(tn, tree)
+    assert ops == ops_ref
+    check_close(val, ref, tn, tree)
+    closed = [l for l in tn.index_table if l not in tn.output and tn.carriers(l)][:2]
+    if closed:
+        refs, _, _ = oracle.contract_sliced(tn, tree, closed)
+        vs, _, _ = contract_sliced(tn, tree, closed)
+        check_close(vs, refs, tn, tree, closed)
+        vs2, _, _ = contract_sliced(tn, tree, closed, graph=False, hoist=False)
+        check_close(vs2, refs, tn, tree, closed)
+
+
+def test_circuit_amplitude_sliced_gemm_path():
+    tn = gen.grid_circuit(5, 5, 20, seed=5)
+    tree = best_greedy_tree(tn, trials=4)
+    m = metrics(tree, tn)
+    ss = greedy_slice(tree, tn, min(m.width, 22) - 2, restarts=2)
+    ref, _, _ = oracle.contract_sliced(tn, tree, ss.labels, slice_ids=range(0, 4))
+    plan = SlicedPlan(tn, tree, ss, gemm_min_macs=2 ** 16).bind()
+    kinds = {v["kind"] for v in plan.vertex_info()}
+    plan.run(0, 4)
+    got = plan.result()
+    assert rel_err(got, ref) <= TOL, rel_err(got, ref)
+    # intermediate-level parity on slice 2 for every dependent vertex
+    rec = {}
+    from paper_2002_01935_b200.slicing import slice_assignment
+    asg = slice_assignment(tn, ss, 2)
+    oracle.contract_one(tn, tree, ss.labels, asg, record=rec)
+    for v in [x["ssa"] for x in plan.vertex_info()][-40:]:
+        labels, arr = plan.debug_vertex(2, v)
+        ol, oarr = rec[v]
+        oarr = np.transpose(oarr, [ol.index(l) for l in labels])
+        assert rel_err(arr, oarr) <= TOL, (v, rel_err(arr, oarr))
+    plan.close()
+    print("kinds", kinds)
+
+
+def test_full_amplitude_statevector_and_unitarity():
+    for case in CASES:
+        if "statevector_amplitude" not in case:
+            continue
+        tn, tree = case_objects(case)
+        val, _, _ = contract(tn, tree)
+        assert abs(val - complex(arr_from_json(case["statevector_amplitude"]))) <= TOL * abs(val)
+    # open-leg circuit: sum_x |c_x|^2 = 1 with one plan reused across bitstrings
+    tn = gen.grid_circuit(2, 3, 6, seed=2, simplify=False)
+    # turn the closing projections into open legs
+    nodes, out = [], []
+    for nd in tn.nodes:
+        if len(nd.indices) == 1 and nd.id >= len(tn.nodes) - 6:
+            out.append(nd.indices[0])
+            continue
+        nodes.append(nd)
+    open_tn = TensorNetwork([TensorNode(i, nd.indices, nd.data) for i, nd in enumerate(nodes)],
+                            tn.index_table, tuple(out))
+    from paper_2002_01935_b200.executor import _project
+    tree = greedy_tree(_project(open_tn, "0" * 6))
+    eng = AmplitudeEngine(open_tn, tree)
+    total = 0.0
+    for x in range(64):
+        bits = format(x, "06b")
+        total += abs(eng(bits)) ** 2
+    eng.close()
+    assert abs(total - 1.0) <= 1e-5
+
+
+def test_multi_slice_ranges_and_accumulator():
+    tn = gen.random_regular(30, 3, seed=3)
+    tree = best_greedy_tree(tn, trials=2)
+    labels = list(tn.index_table)[:4]
+    plan = SlicedPlan(tn, tree, labels).bind()
+    plan.run(0, 7)
+    plan.run(7, 16)
+    full = plan.result()
+    ref, _, _ = oracle.contract_sliced(tn, tree, labels)
+    assert rel_err(full, ref) <= TOL
+    plan.reset()
+    plan.run(3, 4)
+    ref3, _, _ = oracle.contract_sliced(tn, tree, labels, slice_ids=[3])
+    assert rel_err(plan.result(), ref3) <= TOL
+    with pytest.raises(ValueError):
+        plan.run(0, 17)
+    plan.close()

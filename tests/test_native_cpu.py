@@ -1,0 +1,92 @@
+"""C-ABI library: loads, exports every declared symbol, and its plan
+compiler reproduces the reference bookkeeping bit-exactly (no GPU needed:
+tnx_plan_create touches no device state)."""
+import os
+import re
+
+import pytest
+
+from conftest import golden_cases, load_golden, REPO
+from _util import case_objects
+from paper_2002_01935_b200 import _native as nat
+from paper_2002_01935_b200.executor import SlicedPlan
+from paper_2002_01935_b200.slicing import sliced_metrics, SliceSet
+from paper_2002_01935_b200.tree import ContractionTree, metrics
+from paper_2002_01935_b200.harness import generators as gen
+
+
+def test_library_exports_every_header_symbol():
+    lib = nat.load()
+    hdr = open(os.path.join(REPO, "include", "tnx.h")).read()
+    declared = set(re.findall(r"\b(tnx_[a-z_0-9]+)\s*\(", hdr))
+    assert declared, "no symbols parsed"
+    assert declared == set(nat.SIGNATURES), declared ^ set(nat.SIGNATURES)
+    for name in declared:
+        assert hasattr(lib, name)
+    assert b"sm_100a" in lib.tnx_version()
+
+
+CASES = golden_cases()
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_native_bookkeeping_matches_reference(case):
+    tn, tree = case_objects(case)
+    for ent in case["sliced"]:
+        plan = SlicedPlan(tn, tree, ent["labels"])
+        assert plan.d == ent["d"]
+        assert plan.ops_per_slice * plan.d == int(ent["Cs"])
+        assert plan.width == ent["Ws"]
+        plan.close()
+
+
+STRUCT = load_golden("reference_structural.json")
+
+
+@pytest.mark.parametrize("case", STRUCT, ids=[c["name"] for c in STRUCT])
+def test_native_bookkeeping_big_configs(case):
+    tn = {"cfg2_5reg100": lambda: gen.random_regular(100, 5, seed=0),
+          "cfg3_lattice20": lambda: gen.square_lattice(20, seed=0),
+          "cfg4_7x7_d40": lambda: gen.grid_circuit(7, 7, 40, seed=0)}[case["name"]]()
+    tree = ContractionTree(case["tree"]["leaves"], [tuple(p) for p in case["tree"]["pairs"]])
+    plan = SlicedPlan(tn, tree, ())
+    assert plan.ops_per_slice == int(case["metrics"]["cost"])  # > 2^64 on cfg2
+    assert plan.width == case["metrics"]["width"]
+    for ent in case["sliced"]:
+        p2 = SlicedPlan(tn, tree, ent["labels"])
+        assert p2.ops_per_slice * p2.d == int(ent["Cs"]) and p2.width == ent["Ws"]
+        p2.close()
+    plan.close()
+
+
+def test_native_errors_mirror_reference():
+    tn = gen.random_regular(10, 3, seed=1)
+    from paper_2002_01935_b200.harness.paths import greedy_tree
+    tree = greedy_tree(tn)
+    with pytest.raises(ValueError):
+        SlicedPlan(tn, tree, ["nope"])
+    with pytest.raises(ValueError):
+        SlicedPlan(tn, tree, ["e0", "e0"])
+    bad = ContractionTree(tuple(range(1, 11)), tree.pairs)
+    with pytest.raises(ValueError):
+        SlicedPlan(tn, bad, ())
+    tn_out = tn.replace(output=("e0",))
+    with pytest.raises(ValueError):
+        SlicedPlan(tn_out, tree, ["e0"])
+
+
+def test_vertex_kinds_and_hoisting():
+    tn = gen.grid_circuit(5, 5, 16, seed=3)
+    from paper_2002_01935_b200.harness.paths import best_greedy_tree
+    from paper_2002_01935_b200.slicing import greedy_slice
+    tree = best_greedy_tree(tn, trials=2)
+    m = metrics(tree, tn)
+    ss = greedy_slice(tree, tn, m.width - 3, restarts=2)
+    plan = SlicedPlan(tn, tree, ss)
+    st = plan.stats()
+    info = plan.vertex_info()
+    assert len(info) == tn.num_nodes - 1
+    assert st["num_hoisted"] == sum(v["hoisted"] for v in info) > 0
+    assert sum(v["macs"] for v in info) == plan.ops_per_slice
+    assert plan.width == sliced_metrics(tree, tn, ss.labels)[0]
+    plan.close()
