@@ -12,9 +12,10 @@
 //   Cim += Ar_h Bi_h + Ar_h Bi_l + Ar_l Bi_h +  Ai_h Br_h + Ai_h Br_l + Ai_l Br_h
 //
 // (the minus uses the instruction descriptor's negate-A bit), accumulating
-// in two FP32 TMEM accumulators (256 columns).  A warp-specialised mbarrier
-// pipeline (TMA producer / MMA issuer) streams 3 stages of 64 KB; the
-// epilogue moves TMEM -> registers (tcgen05.ld) -> interleaved complex64.
+// in FP32 TMEM accumulators.  A warp-specialised mbarrier pipeline (TMA
+// producer / MMA issuer) streams 3 stages of 64 KB; every `promote` k-blocks
+// the partial accumulators are promoted into FP32 registers of 8 epilogue
+// warps (TMEM double-buffered), which finally store interleaved complex64.
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -33,7 +34,7 @@ constexpr int STAGES = 3;
 constexpr int PLANE_BYTES = BM * BK * 4;        // 8 KB per plane tile
 constexpr int STAGE_BYTES = 8 * PLANE_BYTES;    // 4 A planes + 4 B planes
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
-constexpr int TMEM_COLS = 256;
+constexpr int TMEM_COLS = 512;
 constexpr int GROUP_M = 8;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -131,18 +132,33 @@ struct GemmArgs {
   int64_t M, N, batch;
   int32_t num_kb;        // kp / BK
   int32_t tiles_m, tiles_n;
+  int32_t promote;       // k-blocks accumulated in TMEM before promotion
   int64_t rows_a, rows_b;  // batch * M, batch * N (rows per plane)
 };
 
-__global__ void __launch_bounds__(128, 1)
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+
+// Warp roles: 0 = TMA producer, 1 = MMA issuer, 2..9 = promotion/epilogue.
+// Tensor-core accumulation rounds toward zero, so its error grows with the
+// number of MMAs folded into one accumulator.  Every `promote` k-blocks the
+// MMA issuer switches to the other TMEM accumulator set (double buffered,
+// 2 x 256 columns) while the epilogue warps add the finished set into FP32
+// registers with round-to-nearest ("promotion", as done for FP8 GEMMs).
+constexpr int NUM_THREADS = 320;
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_c64_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a,
                            const __grid_constant__ CUtensorMap tm_b, const GemmArgs g) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  // bars[0..S) full, bars[S..2S) empty, bars[2S] done; tmem slot after
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 1);
+  // [0,S) full  [S,2S) empty  [2S,2S+2) tmem_full  [2S+2,2S+4) tmem_empty
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = bars + 2 * STAGES + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -169,7 +185,10 @@ __global__ void __launch_bounds__(128, 1)
       mbar_init(smem_addr(&bars[s]), 1);
       mbar_init(smem_addr(&bars[STAGES + s]), 1);
     }
-    mbar_init(smem_addr(&bars[2 * STAGES]), 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(smem_addr(&tfull[s]), 1);
+      mbar_init(smem_addr(&tempty[s]), 8);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -179,109 +198,141 @@ __global__ void __launch_bounds__(128, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int nkb = g.num_kb;
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer ----------------
-    const int row_a = (int)(b * g.M + (int64_t)tm * BM);
-    const int row_b = (int)(b * g.N + (int64_t)tn * BN);
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int kb = 0; kb < nkb; ++kb) {
-      mbar_wait(smem_addr(&bars[STAGES + stage]), phase ^ 1u);
-      const uint32_t full = smem_addr(&bars[stage]);
-      mbar_expect_tx(full, STAGE_BYTES);
-      unsigned char* sbase = smem + stage * STAGE_BYTES;
-      const int kc = kb * BK;
+  const int P = g.promote;
+  const int rounds = (nkb + P - 1) / P;
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      const int row_a = (int)(b * g.M + (int64_t)tm * BM);
+      const int row_b = (int)(b * g.N + (int64_t)tn * BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(smem_addr(&bars[STAGES + stage]), phase ^ 1u);
+        const uint32_t full = smem_addr(&bars[stage]);
+        mbar_expect_tx(full, STAGE_BYTES);
+        unsigned char* sbase = smem + stage * STAGE_BYTES;
+        const int kc = kb * BK;
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        tma_load_2d(smem_addr(sbase + p * PLANE_BYTES), &tm_a, full, kc,
-                    (int)(p * g.rows_a + row_a));
-        tma_load_2d(smem_addr(sbase + (4 + p) * PLANE_BYTES), &tm_b, full, kc,
-                    (int)(p * g.rows_b + row_b));
-      }
-      if (++stage == STAGES) {
-        stage = 0;
-        phase ^= 1u;
+        for (int p = 0; p < 4; ++p) {
+          tma_load_2d(smem_addr(sbase + p * PLANE_BYTES), &tm_a, full, kc,
+                      (int)(p * g.rows_a + row_a));
+          tma_load_2d(smem_addr(sbase + (4 + p) * PLANE_BYTES), &tm_b, full, kc,
+                      (int)(p * g.rows_b + row_b));
+        }
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1u;
+        }
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer ----------------
-    const uint32_t d_re = tmem_base;
-    const uint32_t d_im = tmem_base + BN;
-    constexpr uint32_t ID_POS = idesc_tf32(false);
-    constexpr uint32_t ID_NEG = idesc_tf32(true);
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int kb = 0; kb < nkb; ++kb) {
-      mbar_wait(smem_addr(&bars[stage]), phase);
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      constexpr uint32_t ID_POS = idesc_tf32(false);
+      constexpr uint32_t ID_NEG = idesc_tf32(true);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int r = 0; r < rounds; ++r) {
+        const int set = r & 1;
+        mbar_wait(smem_addr(&tempty[set]), ((uint32_t)(r >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t d_re = tmem_base + set * 256;
+        const uint32_t d_im = d_re + BN;
+        const int kb0 = r * P;
+        const int kb1 = min(nkb, kb0 + P);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(smem_addr(&bars[stage]), phase);
+          tc_fence_after();
+          const uint32_t sb = smem_addr(smem + stage * STAGE_BYTES);
+#pragma unroll
+          for (int ks = 0; ks < BK / 8; ++ks) {
+            const uint32_t koff = ks * 32;  // bytes within the 64 B swizzled row
+            const uint64_t ar_h = umma_desc_sw64(sb + 0 * PLANE_BYTES + koff);
+            const uint64_t ar_l = umma_desc_sw64(sb + 1 * PLANE_BYTES + koff);
+            const uint64_t ai_h = umma_desc_sw64(sb + 2 * PLANE_BYTES + koff);
+            const uint64_t ai_l = umma_desc_sw64(sb + 3 * PLANE_BYTES + koff);
+            const uint64_t br_h = umma_desc_sw64(sb + 4 * PLANE_BYTES + koff);
+            const uint64_t br_l = umma_desc_sw64(sb + 5 * PLANE_BYTES + koff);
+            const uint64_t bi_h = umma_desc_sw64(sb + 6 * PLANE_BYTES + koff);
+            const uint64_t bi_l = umma_desc_sw64(sb + 7 * PLANE_BYTES + koff);
+            const uint32_t acc0 = (kb > kb0 || ks > 0) ? 1u : 0u;
+            // small cross terms first
+            umma_tf32(d_re, ar_h, br_l, ID_POS, acc0);
+            umma_tf32(d_re, ar_l, br_h, ID_POS, 1u);
+            umma_tf32(d_re, ai_h, bi_l, ID_NEG, 1u);
+            umma_tf32(d_re, ai_l, bi_h, ID_NEG, 1u);
+            umma_tf32(d_re, ar_h, br_h, ID_POS, 1u);
+            umma_tf32(d_re, ai_h, bi_h, ID_NEG, 1u);
+            umma_tf32(d_im, ar_h, bi_l, ID_POS, acc0);
+            umma_tf32(d_im, ar_l, bi_h, ID_POS, 1u);
+            umma_tf32(d_im, ai_h, br_l, ID_POS, 1u);
+            umma_tf32(d_im, ai_l, br_h, ID_POS, 1u);
+            umma_tf32(d_im, ar_h, bi_h, ID_POS, 1u);
+            umma_tf32(d_im, ai_h, br_h, ID_POS, 1u);
+          }
+          umma_commit(smem_addr(&bars[STAGES + stage]));  // frees the smem stage
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        umma_commit(smem_addr(&tfull[set]));  // this accumulator set is complete
+      }
+    }
+  } else {
+    // ---------------- promotion + epilogue (8 warps) ----------------
+    const int q = warp & 3;          // TMEM lane quarter this warp may access
+    const int h = (warp - 2) >> 2;   // column half
+    float mre[64], mim[64];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) {
+      mre[j] = 0.f;
+      mim[j] = 0.f;
+    }
+    const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16) + h * 64;
+    for (int r = 0; r < rounds; ++r) {
+      const int set = r & 1;
+      mbar_wait(smem_addr(&tfull[set]), (uint32_t)(r >> 1) & 1u);
       tc_fence_after();
-      const uint32_t sb = smem_addr(smem + stage * STAGE_BYTES);
+      const uint32_t t0 = lane_base + set * 256;
 #pragma unroll
-      for (int ks = 0; ks < BK / 8; ++ks) {
-        const uint32_t koff = ks * 32;  // bytes within the 64 B swizzled row
-        const uint64_t ar_h = umma_desc_sw64(sb + 0 * PLANE_BYTES + koff);
-        const uint64_t ar_l = umma_desc_sw64(sb + 1 * PLANE_BYTES + koff);
-        const uint64_t ai_h = umma_desc_sw64(sb + 2 * PLANE_BYTES + koff);
-        const uint64_t ai_l = umma_desc_sw64(sb + 3 * PLANE_BYTES + koff);
-        const uint64_t br_h = umma_desc_sw64(sb + 4 * PLANE_BYTES + koff);
-        const uint64_t br_l = umma_desc_sw64(sb + 5 * PLANE_BYTES + koff);
-        const uint64_t bi_h = umma_desc_sw64(sb + 6 * PLANE_BYTES + koff);
-        const uint64_t bi_l = umma_desc_sw64(sb + 7 * PLANE_BYTES + koff);
-        const uint32_t acc0 = (kb | ks) ? 1u : 0u;
-        // small cross terms first
-        umma_tf32(d_re, ar_h, br_l, ID_POS, acc0);
-        umma_tf32(d_re, ar_l, br_h, ID_POS, 1u);
-        umma_tf32(d_re, ai_h, bi_l, ID_NEG, 1u);
-        umma_tf32(d_re, ai_l, bi_h, ID_NEG, 1u);
-        umma_tf32(d_re, ar_h, br_h, ID_POS, 1u);
-        umma_tf32(d_re, ai_h, bi_h, ID_NEG, 1u);
-        umma_tf32(d_im, ar_h, bi_l, ID_POS, acc0);
-        umma_tf32(d_im, ar_l, bi_h, ID_POS, 1u);
-        umma_tf32(d_im, ai_h, br_l, ID_POS, 1u);
-        umma_tf32(d_im, ai_l, br_h, ID_POS, 1u);
-        umma_tf32(d_im, ar_h, bi_h, ID_POS, 1u);
-        umma_tf32(d_im, ai_h, br_h, ID_POS, 1u);
+      for (int j = 0; j < 4; ++j) {
+        uint32_t re[16], im[16];
+        tmem_ld16(t0 + j * 16, re);
+        tmem_ld16(t0 + BN + j * 16, im);
+        tmem_wait_ld();
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          mre[j * 16 + t] += __uint_as_float(re[t]);
+          mim[j * 16 + t] += __uint_as_float(im[t]);
+        }
       }
-      umma_commit(smem_addr(&bars[STAGES + stage]));  // frees the smem stage
-      if (++stage == STAGES) {
-        stage = 0;
-        phase ^= 1u;
-      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_addr(&tempty[set]));
     }
-    umma_commit(smem_addr(&bars[2 * STAGES]));  // accumulators complete
-  }
-  __syncwarp();
-
-  // ---------------- epilogue: TMEM -> registers -> complex64 ----------------
-  mbar_wait(smem_addr(&bars[2 * STAGES]), 0);
-  tc_fence_after();
-  const int64_t row = (int64_t)tm * BM + warp * 32 + lane;
-  const uint32_t lane_base = tmem_base + ((uint32_t)(warp * 32) << 16);
-  float2* orow = g.out + ((int64_t)b * g.M + row) * g.N;
-  const bool row_ok = row < g.M;
-#pragma unroll 1
-  for (int c = 0; c < BN; c += 16) {
-    uint32_t re[16], im[16];
-    tmem_ld16(lane_base + c, re);
-    tmem_ld16(lane_base + BN + c, im);
-    tmem_wait_ld();
-    const int64_t col = (int64_t)tn * BN + c;
-    if (row_ok) {
-      if (col + 16 <= g.N && (g.N & 1) == 0) {
-        float4* dst = reinterpret_cast<float4*>(orow + col);
+    const int64_t row = (int64_t)tm * BM + q * 32 + lane;
+    if (row < g.M) {
+      float2* orow = g.out + ((int64_t)b * g.M + row) * g.N;
+      const int64_t col0 = (int64_t)tn * BN + h * 64;
+      if (col0 + 64 <= g.N && (g.N & 1) == 0) {
+        float4* dst = reinterpret_cast<float4*>(orow + col0);
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          dst[j] = make_float4(__uint_as_float(re[2 * j]), __uint_as_float(im[2 * j]),
-                               __uint_as_float(re[2 * j + 1]), __uint_as_float(im[2 * j + 1]));
+        for (int j = 0; j < 32; ++j)
+          dst[j] = make_float4(mre[2 * j], mim[2 * j], mre[2 * j + 1], mim[2 * j + 1]);
       } else {
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if (col + j < g.N) orow[col + j] = make_float2(__uint_as_float(re[j]), __uint_as_float(im[j]));
+        for (int j = 0; j < 64; ++j)
+          if (col0 + j < g.N) orow[col0 + j] = make_float2(mre[j], mim[j]);
       }
     }
   }
+  __syncwarp();
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
+    tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"(TMEM_COLS)
                  : "memory");
@@ -370,12 +421,13 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
   a.num_kb = (int32_t)(g.kp / BK);
   a.tiles_m = (int32_t)((g.M + BM - 1) / BM);
   a.tiles_n = (int32_t)((g.N + BN - 1) / BN);
+  a.promote = g.promote > 0 ? g.promote : 2;
   a.rows_a = g.batch * g.M;
   a.rows_b = g.batch * g.N;
   dim3 grid((unsigned)(a.tiles_m * a.tiles_n), (unsigned)g.batch);
   const CUtensorMap* ta = reinterpret_cast<const CUtensorMap*>(g.tmap_a);
   const CUtensorMap* tb = reinterpret_cast<const CUtensorMap*>(g.tmap_b);
-  gemm_c64_3xtf32_kernel<<<grid, 128, SMEM_BYTES, st>>>(*ta, *tb, a);
+  gemm_c64_3xtf32_kernel<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(*ta, *tb, a);
   return cudaGetLastError();
 }
 

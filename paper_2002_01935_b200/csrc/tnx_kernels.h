@@ -95,6 +95,7 @@ struct GemmPlan {
   float2* out;
   int64_t M, N, kp, batch;
   int32_t ok;
+  int32_t promote;        // k-blocks (of 16) per TMEM accumulation round
 };
 // Build tensor maps for planes laid out as [4][batch][M|N][kp] fp32.
 int gemm_prepare(GemmPlan* g, const float* a_planes, const float* b_planes, float2* out,
