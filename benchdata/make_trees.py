@@ -1,0 +1,81 @@
+"""Produce the benchmark contraction trees with the REFERENCE's own drivers.
+
+Run in the build container (needs /root/reference):
+
+    python benchdata/make_trees.py [config ...]
+
+Trees come from ``hypertn.drivers.greedy.greedy_sample`` (best of N random
+(alpha, tau) shots -- the harness stand-in for the SPEC hyper-tuner, SURVEY.md
+§2 row 12) and ``hypertn.tree.minfill_order`` -> ``tree_from_edge_order``.
+The networks themselves are regenerated deterministically on the GPU box by
+``paper_2002_01935_b200.harness.generators``; only the SSA path and its
+bookkeeping are stored here.
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(HERE)
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+
+from hypertn import network as rnet  # noqa: E402
+from hypertn import tree as rtree  # noqa: E402
+from hypertn.drivers import greedy as rgreedy  # noqa: E402
+
+from paper_2002_01935_b200.harness import generators as gen  # noqa: E402
+
+CONFIGS = {
+    "cfg2_5reg100": (lambda: gen.random_regular(100, 5, seed=0), 48, False),
+    "cfg3_lattice20": (lambda: gen.square_lattice(20, seed=0), 24, True),
+    "cfg4_7x7_d40": (lambda: gen.grid_circuit(7, 7, 40, seed=0), 48, False),
+    "cfg5_syc53_m12": (lambda: gen.sycamore_circuit(12, seed=0), 48, False),
+}
+
+
+def to_ref(tn):
+    return rnet.TensorNetwork([rnet.TensorNode(nd.id, nd.indices, None) for nd in tn.nodes],
+                              dict(tn.index_table), tn.output)
+
+
+def search(name, make, shots, minfill):
+    tn = to_ref(make())
+    rng = np.random.default_rng(2002)
+    best = None
+    t0 = time.time()
+    cands = [("greedy", 1.0, 0.0, 0)]
+    for s in range(shots):
+        cands.append(("greedy", float(rng.uniform(0.0, 2.0)), float(rng.choice([0.0, 0.01, 0.05, 0.2])), s + 1))
+    if minfill:
+        for s in range(4):
+            cands.append(("minfill", 0.0, 0.0, s))
+    for kind, alpha, tau, seed in cands:
+        if kind == "greedy":
+            tree = rgreedy.greedy_sample(tn, alpha, tau, seed)
+        else:
+            tree = rtree.tree_from_edge_order(rtree.minfill_order(tn, seed), tn, seed)
+        m = rtree.metrics(tree, tn)
+        key = (m.log10_cost, m.width)
+        if best is None or key < best[0]:
+            best = (key, tree, m, {"driver": kind, "alpha": alpha, "tau": tau, "seed": seed})
+    key, tree, m, how = best
+    print(f"{name}: W={m.width} log10C={m.log10_cost:.3f} via {how} ({time.time() - t0:.1f}s)")
+    return {"name": name, "driver": how, "shots": len(cands),
+            "tree": {"leaves": list(tree.leaves), "pairs": [list(p) for p in tree.pairs]},
+            "width": m.width, "cost": str(m.cost), "log10_cost": m.log10_cost}
+
+
+def main(names):
+    for name in names:
+        make, shots, minfill = CONFIGS[name]
+        rec = search(name, make, shots, minfill)
+        with open(os.path.join(HERE, f"{name}.tree.json"), "w") as fh:
+            json.dump(rec, fh)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or list(CONFIGS))

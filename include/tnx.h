@@ -144,6 +144,13 @@ int tnx_vertex_info_get(void* plan, int32_t index, tnx_vertex_info* out);
 int tnx_debug_vertex(void* plan, uint64_t s, int32_t v, float* out_c64,
                      int64_t out_elems, int32_t* layout_labels, int32_t* rank_out);
 
+/* Profiling: run slice s (not accumulated) launch by launch on the plan's
+ * stream with CUDA events around every kernel; fills up to max_launches
+ * entries (type: 0 gather, 1 simt, 2 pack, 3 gemm, 4 accum; vertex = SSA id
+ * or -1; ms = event-timed duration) and returns the count in *count. */
+int tnx_profile_slice(void* plan, uint64_t s, int32_t* types, int32_t* vertices, float* ms,
+                      int32_t max_launches, int32_t* count);
+
 /* Synchronise the plan's device; returns a CUDA error if one is pending. */
 int tnx_synchronize(void* plan);
 

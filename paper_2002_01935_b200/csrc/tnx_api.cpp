@@ -947,6 +947,44 @@ int tnx_debug_vertex(void* plan, uint64_t s, int32_t v, float* out_c64, int64_t 
   return TNX_OK;
 }
 
+int tnx_profile_slice(void* plan, uint64_t s, int32_t* types, int32_t* vertices, float* ms,
+                      int32_t max_launches, int32_t* count) {
+  Plan& P = *static_cast<Plan*>(plan);
+  if (!P.bound) return fail(TNX_ERR_STATE, "not bound");
+  if ((u128)s >= P.d) return fail(TNX_ERR_INVALID, "slice out of range");
+  TNX_CUDA(cudaSetDevice(P.device));
+  cudaStream_t st = P.own;
+  const int n = (int)P.slice_launches.size();
+  std::vector<cudaEvent_t> ev(n + 1);
+  for (auto& e : ev) TNX_CUDA(cudaEventCreate(&e));
+  cudaError_t e = launch_set_counter(P.counter, s, st);
+  if (e != cudaSuccess) return fail(TNX_ERR_CUDA, cudaGetErrorString(e));
+  TNX_CUDA(cudaEventRecord(ev[0], st));
+  int done = 0;
+  for (int i = 0; i < n; ++i) {
+    const Launch& L = P.slice_launches[i];
+    if (L.type == L_ACCUM) break;  // profiling does not accumulate
+    std::vector<Launch> one{L};
+    int rc = run_launches(P, one, st, -1);
+    if (rc) return rc;
+    TNX_CUDA(cudaEventRecord(ev[i + 1], st));
+    done = i + 1;
+  }
+  TNX_CUDA(cudaStreamSynchronize(st));
+  int m = std::min(done, (int)max_launches);
+  for (int i = 0; i < m; ++i) {
+    const Launch& L = P.slice_launches[i];
+    types[i] = L.type == L_GATHER ? 0 : L.type == L_SIMT ? 1 : L.type == L_PACK ? 2 : L.type == L_GEMM ? 3 : 4;
+    vertices[i] = L.vertex;
+    float t = 0.f;
+    TNX_CUDA(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
+    ms[i] = t;
+  }
+  for (auto& x : ev) cudaEventDestroy(x);
+  *count = m;
+  return TNX_OK;
+}
+
 int tnx_synchronize(void* plan) {
   Plan& P = *static_cast<Plan*>(plan);
   TNX_CUDA(cudaSetDevice(P.device));
