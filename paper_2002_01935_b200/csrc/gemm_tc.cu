@@ -19,6 +19,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include "tnx_kernels.h"
@@ -133,6 +134,8 @@ struct GemmArgs {
   int32_t num_kb;        // kp / BK
   int32_t tiles_m, tiles_n;
   int32_t promote;       // k-blocks accumulated in TMEM before promotion
+  int32_t kb_per_split;  // split-K: k-blocks per CTA along grid.z
+  float2* partial;       // split-K workspace [splits][batch][M][N] (nullptr: 1 split)
   int64_t rows_a, rows_b;  // batch * M, batch * N (rows per plane)
 };
 
@@ -197,9 +200,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int nkb = g.num_kb;
+  const int kb_begin = blockIdx.z * g.kb_per_split;
+  const int nkb = min(g.num_kb - kb_begin, g.kb_per_split);  // k-blocks of this CTA
   const int P = g.promote;
   const int rounds = (nkb + P - 1) / P;
+  float2* const out = g.partial ? g.partial + (int64_t)blockIdx.z * g.batch * g.M * g.N : g.out;
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
@@ -212,7 +217,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t full = smem_addr(&bars[stage]);
         mbar_expect_tx(full, STAGE_BYTES);
         unsigned char* sbase = smem + stage * STAGE_BYTES;
-        const int kc = kb * BK;
+        const int kc = (kb_begin + kb) * BK;
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
           tma_load_2d(smem_addr(sbase + p * PLANE_BYTES), &tm_a, full, kc,
@@ -314,7 +319,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     const int64_t row = (int64_t)tm * BM + q * 32 + lane;
     if (row < g.M) {
-      float2* orow = g.out + ((int64_t)b * g.M + row) * g.N;
+      float2* orow = out + ((int64_t)b * g.M + row) * g.N;
       const int64_t col0 = (int64_t)tn * BN + h * 64;
       if (col0 + 64 <= g.N && (g.N & 1) == 0) {
         float4* dst = reinterpret_cast<float4*>(orow + col0);
@@ -391,8 +396,15 @@ int gemm_init_attributes(char* err, size_t errlen) {
 }
 
 int gemm_prepare(GemmPlan* g, const float* a_planes, const float* b_planes, float2* out,
-                 int64_t batch, int64_t M, int64_t N, int64_t kp, char* err, size_t errlen) {
+                 int64_t batch, int64_t M, int64_t N, int64_t kp, int splits, float2* partial,
+                 char* err, size_t errlen) {
   std::memset(g, 0, sizeof(*g));
+  g->splits = splits;
+  g->partial = partial;
+  if (splits > 1 && (!partial || (batch * M * N) % 2 != 0)) {
+    snprintf(err, errlen, "gemm: split-K needs a workspace and an even output size");
+    return 1;
+  }
   if (kp % BK != 0) {
     snprintf(err, errlen, "gemm: kp=%lld not a multiple of %d", (long long)kp, BK);
     return 1;
@@ -412,6 +424,31 @@ int gemm_prepare(GemmPlan* g, const float* a_planes, const float* b_planes, floa
   return 0;
 }
 
+__global__ void splitk_reduce_kernel(const float4* __restrict__ part, float4* __restrict__ out,
+                                     int64_t n4, int64_t stride4, int splits) {
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += step) {
+    float4 a = part[i];
+    for (int s = 1; s < splits; ++s) {
+      float4 v = part[i + s * stride4];
+      a.x += v.x;
+      a.y += v.y;
+      a.z += v.z;
+      a.w += v.w;
+    }
+    out[i] = a;
+  }
+}
+
+int gemm_choose_splits(int64_t batch, int64_t M, int64_t N, int64_t kp) {
+  const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * batch;
+  const int64_t nkb = kp / BK;
+  if (tiles >= 148) return 1;
+  int64_t s = 148 / tiles;
+  s = std::min<int64_t>(s, nkb / 8);  // at least 8 k-blocks (K=128) per CTA
+  return (int)std::max<int64_t>(1, s);
+}
+
 cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
   GemmArgs a;
   a.out = g.out;
@@ -422,12 +459,24 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
   a.tiles_m = (int32_t)((g.M + BM - 1) / BM);
   a.tiles_n = (int32_t)((g.N + BN - 1) / BN);
   a.promote = g.promote > 0 ? g.promote : 2;
+  const int splits = g.splits > 1 ? g.splits : 1;
+  a.kb_per_split = (a.num_kb + splits - 1) / splits;
+  a.partial = splits > 1 ? g.partial : nullptr;
   a.rows_a = g.batch * g.M;
   a.rows_b = g.batch * g.N;
-  dim3 grid((unsigned)(a.tiles_m * a.tiles_n), (unsigned)g.batch);
+  const int zs = (a.num_kb + a.kb_per_split - 1) / a.kb_per_split;
+  dim3 grid((unsigned)(a.tiles_m * a.tiles_n), (unsigned)g.batch, (unsigned)zs);
   const CUtensorMap* ta = reinterpret_cast<const CUtensorMap*>(g.tmap_a);
   const CUtensorMap* tb = reinterpret_cast<const CUtensorMap*>(g.tmap_b);
   gemm_c64_3xtf32_kernel<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(*ta, *tb, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || zs == 1) return e;
+  const int64_t n = g.batch * g.M * g.N;  // complex elements
+  if (n % 2 != 0) return cudaErrorInvalidValue;
+  const int64_t n4 = n / 2;
+  int blocks = (int)std::min<int64_t>((n4 + 255) / 256, 148 * 16);
+  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(g.partial),
+                                               reinterpret_cast<float4*>(g.out), n4, n4, zs);
   return cudaGetLastError();
 }
 

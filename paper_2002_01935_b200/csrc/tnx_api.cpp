@@ -110,6 +110,7 @@ struct Vertex {
   int nsplit = 0;
   int64_t chunk = 0;
   int blk_apl = -1, blk_bpl = -1, blk_part = -1;
+  int splits = 1;
   int64_t tab_off = -1;  // element offset in the sum-table buffer
 };
 
@@ -515,6 +516,8 @@ int compile(Plan& P, const tnx_plan_desc* D) {
     if (v.kind == VK_GEMM) {
       v.blk_apl = add_block(ph, 16 * v.B * v.M * v.kp, st, st);
       v.blk_bpl = add_block(ph, 16 * v.B * v.N * v.kp, st, st);
+      v.splits = ((v.B * v.M * v.N) % 2 == 0) ? gemm_choose_splits(v.B, v.M, v.N, v.kp) : 1;
+      if (v.splits > 1) v.blk_part = add_block(ph, 8 * (int64_t)v.splits * v.B * v.M * v.N, st, st);
     }
   }
   P.persist_bytes = std::max<int64_t>(persist_off, kAlign);
@@ -599,7 +602,8 @@ int lower(Plan& P) {
         P.packs.push_back(pb);
         out.push_back({L_PACK, (int)P.packs.size() - 1, v.ssa});
         GemmPlan g;
-        if (gemm_prepare(&g, apl, bpl, P.ptr(z), v.B, v.M, v.N, v.kp, ebuf, sizeof(ebuf)))
+        float2* part = v.splits > 1 ? reinterpret_cast<float2*>(P.block_ptr(phase, v.blk_part)) : nullptr;
+        if (gemm_prepare(&g, apl, bpl, P.ptr(z), v.B, v.M, v.N, v.kp, v.splits, part, ebuf, sizeof(ebuf)))
           return fail(TNX_ERR_CUDA, std::string("vertex ") + std::to_string(v.ssa) + ": " + ebuf);
         P.gemms.push_back(g);
         out.push_back({L_GEMM, (int)P.gemms.size() - 1, v.ssa});
@@ -887,7 +891,7 @@ int tnx_stats_get(void* plan, tnx_stats* s) {
   for (int k : P.slice_order) {
     if (P.V[k].kind == VK_GEMM) {
       ++ng;
-      launches += 3;
+      launches += P.V[k].splits > 1 ? 4 : 3;
     } else {
       ++ns;
       launches += P.V[k].kind == VK_SIMT_S ? 2 : 1;
@@ -1030,13 +1034,17 @@ int tnx_gemm_c64(const void* A, const void* B, void* C, int64_t batch, int64_t M
   if (e != cudaSuccess) return fail(TNX_ERR_CUDA, cudaGetErrorString(e));
   (void)precision;
   GemmPlan g;
-  if (gemm_prepare(&g, apl, bpl, static_cast<float2*>(C), batch, M, N, kp, ebuf, sizeof(ebuf)))
+  int splits = ((batch * M * N) % 2 == 0) ? gemm_choose_splits(batch, M, N, kp) : 1;
+  float2* part = nullptr;
+  if (splits > 1) TNX_CUDA(cudaMalloc(&part, 8 * (size_t)splits * batch * M * N));
+  if (gemm_prepare(&g, apl, bpl, static_cast<float2*>(C), batch, M, N, kp, splits, part, ebuf, sizeof(ebuf)))
     return fail(TNX_ERR_CUDA, ebuf);
   e = launch_gemm(g, st);
   if (e != cudaSuccess) return fail(TNX_ERR_CUDA, cudaGetErrorString(e));
   TNX_CUDA(cudaStreamSynchronize(st));
   cudaFree(apl);
   cudaFree(bpl);
+  if (part) cudaFree(part);
   return TNX_OK;
 }
 

@@ -96,10 +96,14 @@ struct GemmPlan {
   int64_t M, N, kp, batch;
   int32_t ok;
   int32_t promote;        // k-blocks (of 16) per TMEM accumulation round
+  int32_t splits;         // split-K factor (1 = none)
+  float2* partial;        // split-K workspace [splits][batch][M][N]
 };
 // Build tensor maps for planes laid out as [4][batch][M|N][kp] fp32.
 int gemm_prepare(GemmPlan* g, const float* a_planes, const float* b_planes, float2* out,
-                 int64_t batch, int64_t M, int64_t N, int64_t kp, char* err, size_t errlen);
+                 int64_t batch, int64_t M, int64_t N, int64_t kp, int splits, float2* partial,
+                 char* err, size_t errlen);
+int gemm_choose_splits(int64_t batch, int64_t M, int64_t N, int64_t kp);
 cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st);
 int gemm_init_attributes(char* err, size_t errlen);
 

@@ -61,7 +61,7 @@ def test_gemm_kernel_vs_numpy():
     from paper_2002_01935_b200 import _native as nat
     lib = nat.load()
     for (b, m, n, k) in [(1, 128, 128, 16), (1, 256, 384, 64), (2, 200, 136, 40), (1, 1024, 512, 1000),
-                         (3, 128, 256, 8)]:
+                         (3, 128, 256, 8), (1, 256, 128, 65536), (2, 130, 132, 20000)]:
         A = (rng.standard_normal((b, m, k)) + 1j * rng.standard_normal((b, m, k))).astype(np.complex64)
         B = (rng.standard_normal((b, n, k)) + 1j * rng.standard_normal((b, n, k))).astype(np.complex64)
         ta = torch.from_numpy(A).cuda()
