@@ -55,7 +55,8 @@ enum { TNX_LOC_HOST = 0, TNX_LOC_DEVICE = 1 };
 /* Plan flags. */
 enum {
   TNX_FLAG_NO_GRAPH = 1u << 0,   /* launch per-slice steps directly (debug) */
-  TNX_FLAG_NO_HOIST = 1u << 1    /* recompute slice-invariant subtrees per slice */
+  TNX_FLAG_NO_HOIST = 1u << 1,   /* recompute slice-invariant subtrees per slice */
+  TNX_FLAG_NO_TILED_PACK = 1u << 2  /* GEMM operands via the gather pack kernel only */
 };
 
 /*

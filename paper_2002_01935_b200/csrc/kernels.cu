@@ -11,6 +11,7 @@
 //               tcgen05 GEMM consumes (coalesced along the padded K axis).
 //  K6 accum   : root -> tn.output order, Kahan-compensated complex128
 //               accumulation across slices.
+#include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "tnx_kernels.h"
@@ -251,6 +252,64 @@ __global__ void __launch_bounds__(256) pack_kernel(const PackParams p) {
 
 cudaError_t launch_pack(const PackParams& p, cudaStream_t st) {
   pack_kernel<<<grid_for(p.rows * p.kp, 256, 148 * 32), 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ tiled permute
+__global__ void __launch_bounds__(256) perm_kernel(const PermParams p) {
+  extern __shared__ __align__(16) unsigned char perm_smem[];
+  __shared__ int64_t base_s[64], base_d[64];
+  const int ts = p.ts;
+  const int G = p.group;
+  int32_t* t_src = reinterpret_cast<int32_t*>(perm_smem);
+  int32_t* t_idx = t_src + ts;
+  int32_t* t_dst = t_idx + ts;
+  float2* tile = reinterpret_cast<float2*>(perm_smem + ((size_t)(3 * ts * 4 + 15) & ~(size_t)15));
+  for (int i = threadIdx.x; i < 3 * ts; i += blockDim.x) t_src[i] = p.tab[i];
+  const int64_t nchunks = (p.n_outer + G - 1) / G;
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const int64_t o0 = c * G;
+    const int gcount = (int)(p.n_outer - o0 < (int64_t)G ? p.n_outer - o0 : (int64_t)G);
+    if (threadIdx.x < gcount) {
+      int64_t sb = 0, db = 0;
+      decode2(p.outer, o0 + threadIdx.x, sb, db);
+      base_s[threadIdx.x] = sb;
+      base_d[threadIdx.x] = db;
+    }
+    __syncthreads();
+    // load: source iteration order (innermost source labels fastest)
+    for (int e = threadIdx.x; e < gcount * ts; e += blockDim.x) {
+      const int j = e / ts, t = e - j * ts;
+      tile[j * ts + t_idx[t]] = p.src[base_s[j] + t_src[t]];
+    }
+    __syncthreads();
+    // store: destination order (innermost destination labels fastest)
+    for (int e = threadIdx.x; e < gcount * ts; e += blockDim.x) {
+      const int j = e / ts, t = e - j * ts;
+      const float2 v = tile[j * ts + t];
+      const int64_t off = base_d[j] + t_dst[t];
+      if (p.mode == 0) {
+        static_cast<float2*>(p.dst)[off] = v;
+      } else {
+        float* d = static_cast<float*>(p.dst);
+        const float re_hi = __uint_as_float(__float_as_uint(v.x) & 0xffffe000u);
+        const float im_hi = __uint_as_float(__float_as_uint(v.y) & 0xffffe000u);
+        d[off] = re_hi;
+        d[off + p.plane_stride] = v.x - re_hi;
+        d[off + 2 * p.plane_stride] = im_hi;
+        d[off + 3 * p.plane_stride] = v.y - im_hi;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_perm(const PermParams& p, cudaStream_t st) {
+  const size_t smem = (((size_t)3 * p.ts * 4 + 15) & ~(size_t)15) + (size_t)p.ts * p.group * 8;
+  const int64_t nchunks = (p.n_outer + p.group - 1) / p.group;
+  int blocks = (int)std::min<int64_t>(nchunks, 148 * 8);
+  if (blocks < 1) blocks = 1;
+  perm_kernel<<<blocks, 256, smem, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -114,7 +114,7 @@ struct Vertex {
   int64_t tab_off = -1;  // element offset in the sum-table buffer
 };
 
-enum LaunchType { L_GATHER, L_SIMT, L_PACK, L_GEMM, L_ACCUM };
+enum LaunchType { L_GATHER, L_SIMT, L_PACK, L_GEMM, L_ACCUM, L_PERM };
 struct Launch {
   int type;
   int idx;
@@ -149,6 +149,8 @@ struct Plan {
   int64_t out_size = 1;
   bool too_wide = false;
   std::vector<Int2Off> tables;
+  std::vector<int32_t> ptabs;   // tiled-permutation tables
+  int32_t* d_ptabs = nullptr;
   int64_t max_partial = 0;
 
   // device state
@@ -169,6 +171,7 @@ struct Plan {
   std::vector<Launch> hoist_launches, slice_launches;
   std::vector<SimtParams> simt;
   std::vector<PackParams> packs;
+  std::vector<PermParams> perms;
   std::vector<GemmPlan> gemms;
   AccumParams accum{};
   std::vector<float2> staging;
@@ -179,13 +182,14 @@ struct Plan {
     if (graph) cudaGraphDestroy(graph);
     gexec = nullptr;
     graph = nullptr;
-    void* ptrs[] = {pool, work, persist, partial, d_tabs, d_jobs, acc, comp, counter};
+    void* ptrs[] = {pool, work, persist, partial, d_tabs, d_jobs, acc, comp, counter, d_ptabs};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     pool = nullptr;
     work = persist = nullptr;
     partial = nullptr;
     d_tabs = nullptr;
+    d_ptabs = nullptr;
     d_jobs = nullptr;
     acc = comp = nullptr;
     counter = nullptr;
@@ -527,6 +531,84 @@ int compile(Plan& P, const tnx_plan_desc* D) {
   return TNX_OK;
 }
 
+// Tiled permutation of tensor t into the row-major order `dst` (same label
+// set).  Tables are appended to P.ptabs (tab_off = element offset).  Returns
+// false when the tile would be too large or offsets overflow int32.
+bool build_perm(Plan& P, const TensorLoc& t, const std::vector<int>& dst, int mode,
+                PermParams& pp, int64_t& tab_off, std::string& err) {
+  std::memset(&pp, 0, sizeof(pp));
+  if (t.size >= (int64_t(1) << 31)) return false;
+  std::vector<char> in_tile(P.L, 0);
+  int64_t prod = 1;
+  for (int i = (int)t.labels.size() - 1; i >= 0 && prod < 32; --i) {
+    prod *= P.dims[t.labels[i]];
+    in_tile[t.labels[i]] = 1;
+  }
+  prod = 1;
+  for (int i = (int)dst.size() - 1; i >= 0 && prod < 32; --i) {
+    prod *= P.dims[dst[i]];
+    in_tile[dst[i]] = 1;
+  }
+  std::vector<int> tsrc, tdst, outer;
+  for (int l : t.labels)
+    if (in_tile[l]) tsrc.push_back(l);
+  for (int l : dst) (in_tile[l] ? tdst : outer).push_back(l);
+  const int64_t ts = P.prod(tsrc);
+  if (ts > 4096 || ts < 1) return false;
+  // destination (row-major) strides
+  std::vector<int64_t> dstr(P.L, 0);
+  int64_t s = 1;
+  for (int i = (int)dst.size() - 1; i >= 0; --i) {
+    dstr[dst[i]] = s;
+    s *= P.dims[dst[i]];
+  }
+  // strides within the dst-ordered tile
+  std::vector<int64_t> tstr(P.L, 0);
+  s = 1;
+  for (int i = (int)tdst.size() - 1; i >= 0; --i) {
+    tstr[tdst[i]] = s;
+    s *= P.dims[tdst[i]];
+  }
+  tab_off = (int64_t)P.ptabs.size();
+  P.ptabs.resize(P.ptabs.size() + 3 * ts);
+  int32_t* T_src = P.ptabs.data() + tab_off;
+  int32_t* T_idx = T_src + ts;
+  int32_t* T_dst = T_idx + ts;
+  auto walk = [&](const std::vector<int>& order, auto&& fn) {
+    std::vector<int64_t> dig(order.size(), 0);
+    for (int64_t e = 0; e < ts; ++e) {
+      fn(e, dig);
+      for (int i = (int)order.size() - 1; i >= 0; --i) {
+        if (++dig[i] < P.dims[order[i]]) break;
+        dig[i] = 0;
+      }
+    }
+  };
+  walk(tsrc, [&](int64_t e, const std::vector<int64_t>& dig) {
+    int64_t so = 0, ti = 0;
+    for (size_t i = 0; i < tsrc.size(); ++i) {
+      so += dig[i] * P.stride_in(t, tsrc[i]);
+      ti += dig[i] * tstr[tsrc[i]];
+    }
+    T_src[e] = (int32_t)so;
+    T_idx[e] = (int32_t)ti;
+  });
+  walk(tdst, [&](int64_t e, const std::vector<int64_t>& dig) {
+    int64_t d = 0;
+    for (size_t i = 0; i < tdst.size(); ++i) d += dig[i] * dstr[tdst[i]];
+    T_dst[e] = (int32_t)d;
+  });
+  // outer map: st0 = source stride, st1 = destination stride
+  TensorLoc dl;
+  dl.labels = dst;
+  if (!build_map(P, outer, &t, &dl, pp.outer, err)) return false;
+  pp.n_outer = P.prod(outer);
+  pp.ts = (int32_t)ts;
+  pp.group = (int32_t)std::max<int64_t>(1, std::min<int64_t>(64, 2048 / ts));
+  pp.mode = mode;
+  return true;
+}
+
 int run_launches(Plan& P, const std::vector<Launch>& ls, cudaStream_t st, int stop_vertex) {
   for (const Launch& L : ls) {
     cudaError_t e = cudaSuccess;
@@ -540,6 +622,9 @@ int run_launches(Plan& P, const std::vector<Launch>& ls, cudaStream_t st, int st
       case L_PACK:
         e = launch_pack(P.packs[L.idx], st);
         break;
+      case L_PERM:
+        e = launch_perm(P.perms[L.idx], st);
+        break;
       case L_GEMM:
         e = launch_gemm(P.gemms[L.idx], st);
         break;
@@ -549,7 +634,7 @@ int run_launches(Plan& P, const std::vector<Launch>& ls, cudaStream_t st, int st
         break;
     }
     if (e != cudaSuccess) return fail(TNX_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
-    if (stop_vertex >= 0 && L.vertex == stop_vertex && L.type != L_PACK) break;
+    if (stop_vertex >= 0 && L.vertex == stop_vertex && L.type != L_PACK && L.type != L_PERM) break;
   }
   return TNX_OK;
 }
@@ -560,6 +645,8 @@ int lower(Plan& P) {
   char ebuf[256];
   P.simt.clear();
   P.packs.clear();
+  P.perms.clear();
+  P.ptabs.clear();
   P.gemms.clear();
   P.hoist_launches.clear();
   P.slice_launches.clear();
@@ -575,32 +662,48 @@ int lower(Plan& P) {
       if (v.kind == VK_GEMM) {
         float* apl = reinterpret_cast<float*>(P.block_ptr(phase, v.blk_apl));
         float* bpl = reinterpret_cast<float*>(P.block_ptr(phase, v.blk_bpl));
-        PackParams pa{};
         std::vector<int> rows_a = v.bl;
         rows_a.insert(rows_a.end(), v.ml.begin(), v.ml.end());
-        if (!build_map(P, rows_a, &x, nullptr, pa.row, err) || !build_map(P, v.cl, &x, nullptr, pa.col, err))
-          return fail(TNX_ERR_INVALID, "vertex " + std::to_string(v.ssa) + ": " + err);
-        pa.src = P.ptr(x);
-        pa.dst = apl;
-        pa.rows = v.B * v.M;
-        pa.K = v.K;
-        pa.kp = v.kp;
-        pa.plane_stride = pa.rows * v.kp;
-        PackParams pb{};
         std::vector<int> rows_b = v.bl;
         rows_b.insert(rows_b.end(), v.nl.begin(), v.nl.end());
-        if (!build_map(P, rows_b, &y, nullptr, pb.row, err) || !build_map(P, v.cl, &y, nullptr, pb.col, err))
-          return fail(TNX_ERR_INVALID, "vertex " + std::to_string(v.ssa) + ": " + err);
-        pb.src = P.ptr(y);
-        pb.dst = bpl;
-        pb.rows = v.B * v.N;
-        pb.K = v.K;
-        pb.kp = v.kp;
-        pb.plane_stride = pb.rows * v.kp;
-        P.packs.push_back(pa);
-        out.push_back({L_PACK, (int)P.packs.size() - 1, v.ssa});
-        P.packs.push_back(pb);
-        out.push_back({L_PACK, (int)P.packs.size() - 1, v.ssa});
+        for (int side = 0; side < 2; ++side) {
+          const TensorLoc& src = side == 0 ? x : y;
+          const std::vector<int>& rows = side == 0 ? rows_a : rows_b;
+          float* planes = side == 0 ? apl : bpl;
+          const int64_t nrows = side == 0 ? v.B * v.M : v.B * v.N;
+          bool done = false;
+          if (v.kp == v.K && !(P.flags & TNX_FLAG_NO_TILED_PACK)) {
+            std::vector<int> dst = rows;
+            dst.insert(dst.end(), v.cl.begin(), v.cl.end());
+            PermParams pp;
+            int64_t toff = 0;
+            const size_t mark = P.ptabs.size();
+            if (build_perm(P, src, dst, 1, pp, toff, err)) {
+              pp.src = P.ptr(src);
+              pp.dst = planes;
+              pp.plane_stride = nrows * v.kp;
+              pp.tab = reinterpret_cast<const int32_t*>(toff);  // rebased after upload
+              P.perms.push_back(pp);
+              out.push_back({L_PERM, (int)P.perms.size() - 1, v.ssa});
+              done = true;
+            } else {
+              P.ptabs.resize(mark);
+            }
+          }
+          if (!done) {
+            PackParams pk{};
+            if (!build_map(P, rows, &src, nullptr, pk.row, err) || !build_map(P, v.cl, &src, nullptr, pk.col, err))
+              return fail(TNX_ERR_INVALID, "vertex " + std::to_string(v.ssa) + ": " + err);
+            pk.src = P.ptr(src);
+            pk.dst = planes;
+            pk.rows = nrows;
+            pk.K = v.K;
+            pk.kp = v.kp;
+            pk.plane_stride = nrows * v.kp;
+            P.packs.push_back(pk);
+            out.push_back({L_PACK, (int)P.packs.size() - 1, v.ssa});
+          }
+        }
         GemmPlan g;
         float2* part = v.splits > 1 ? reinterpret_cast<float2*>(P.block_ptr(phase, v.blk_part)) : nullptr;
         if (gemm_prepare(&g, apl, bpl, P.ptr(z), v.B, v.M, v.N, v.kp, v.splits, part, ebuf, sizeof(ebuf)))
@@ -778,6 +881,11 @@ int tnx_bind_leaves(void* plan, const void* const* leaf_data, int32_t dtype, int
     }
     int rc = lower(P);
     if (rc) return rc;
+    if (!P.ptabs.empty()) {
+      TNX_CUDA(cudaMalloc(&P.d_ptabs, P.ptabs.size() * sizeof(int32_t)));
+      TNX_CUDA(cudaMemcpy(P.d_ptabs, P.ptabs.data(), P.ptabs.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+      for (auto& pp : P.perms) pp.tab = P.d_ptabs + reinterpret_cast<intptr_t>(pp.tab);
+    }
     P.bound = true;
   }
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.own;
@@ -891,7 +999,7 @@ int tnx_stats_get(void* plan, tnx_stats* s) {
   for (int k : P.slice_order) {
     if (P.V[k].kind == VK_GEMM) {
       ++ng;
-      launches += P.V[k].splits > 1 ? 4 : 3;
+      launches += P.V[k].splits > 1 ? 4 : 3;  // 2 packs + gemm (+ split-K reduce)
     } else {
       ++ns;
       launches += P.V[k].kind == VK_SIMT_S ? 2 : 1;
@@ -978,7 +1086,8 @@ int tnx_profile_slice(void* plan, uint64_t s, int32_t* types, int32_t* vertices,
   int m = std::min(done, (int)max_launches);
   for (int i = 0; i < m; ++i) {
     const Launch& L = P.slice_launches[i];
-    types[i] = L.type == L_GATHER ? 0 : L.type == L_SIMT ? 1 : L.type == L_PACK ? 2 : L.type == L_GEMM ? 3 : 4;
+    types[i] = L.type == L_GATHER ? 0 : L.type == L_SIMT ? 1 : (L.type == L_PACK || L.type == L_PERM) ? 2
+             : L.type == L_GEMM ? 3 : 4;
     vertices[i] = L.vertex;
     float t = 0.f;
     TNX_CUDA(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));

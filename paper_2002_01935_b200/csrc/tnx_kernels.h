@@ -53,6 +53,24 @@ struct PackParams {
   int64_t plane_stride;   // rows * kp
 };
 
+// Shared-memory tiled permutation (K2).  The tile spans the innermost source
+// labels (coalesced reads) and the innermost destination labels (coalesced
+// writes); `tab` holds three int32 tables of length ts: source offsets and
+// smem slots in source iteration order, destination offsets in destination
+// order.  `group` outer indices are processed per tile pass.
+struct PermParams {
+  IdxMap outer;           // outer index -> (src base st0, dst base st1)
+  const int32_t* tab;     // [3][ts]
+  const float2* src;
+  void* dst;              // float planes (mode 1) or float2 (mode 0)
+  int64_t n_outer;
+  int64_t plane_stride;   // mode 1: elements per plane
+  int32_t ts;
+  int32_t group;
+  int32_t mode;           // 0: complex64 copy, 1: split-TF32 planes
+  int32_t pad;
+};
+
 constexpr int kMaxLeafRank = 16;
 struct GatherJob {
   int64_t src;            // element offset in the leaf pool
@@ -83,6 +101,7 @@ cudaError_t launch_gather(const GatherJob* jobs, int njobs, const float2* leaf_p
                           const unsigned long long* slice_counter, cudaStream_t st);
 cudaError_t launch_simt(const SimtParams& p, cudaStream_t st);
 cudaError_t launch_pack(const PackParams& p, cudaStream_t st);
+cudaError_t launch_perm(const PermParams& p, cudaStream_t st);
 cudaError_t launch_accum(const AccumParams& p, cudaStream_t st);
 cudaError_t launch_set_counter(unsigned long long* counter, unsigned long long v, cudaStream_t st);
 cudaError_t launch_convert_c128(const double2* src, float2* dst, int64_t n, cudaStream_t st);

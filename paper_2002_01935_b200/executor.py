@@ -57,7 +57,7 @@ class SlicedPlan:
     """
 
     def __init__(self, tn, tree, slice_set=(), device=0, precision="3xtf32", graph=True,
-                 hoist=True, gemm_min_macs=0.0):
+                 hoist=True, gemm_min_macs=0.0, tiled_pack=True):
         lib = nat.load()
         self.tn = tn
         self.tree = tree
@@ -89,7 +89,8 @@ class SlicedPlan:
             ranks=_i32(ranks), leaf_labels=_i32(leaf_labels), pairs=_i32(pairs),
             out=_i32([lid[l] for l in tn.output]), sl=_i32([lid[l] for l in self.sliced]))
         k = self._keep
-        flags = (0 if graph else nat.FLAG_NO_GRAPH) | (0 if hoist else nat.FLAG_NO_HOIST)
+        flags = ((0 if graph else nat.FLAG_NO_GRAPH) | (0 if hoist else nat.FLAG_NO_HOIST)
+                 | (0 if tiled_pack else nat.FLAG_NO_TILED_PACK))
         if precision not in PRECISIONS:
             raise ValueError(f"unknown precision {precision!r}; choose from {sorted(PRECISIONS)}")
         self.precision = precision

@@ -162,3 +162,20 @@ def test_multi_slice_ranges_and_accumulator():
     with pytest.raises(ValueError):
         plan.run(0, 17)
     plan.close()
+
+
+def test_tiled_pack_matches_gather_pack():
+    tn = gen.grid_circuit(5, 5, 24, seed=7)
+    tree = best_greedy_tree(tn, trials=3)
+    m = metrics(tree, tn)
+    ss = greedy_slice(tree, tn, min(m.width, 23) - 1, restarts=1)
+    vals = []
+    for tiled in (True, False):
+        plan = SlicedPlan(tn, tree, ss, gemm_min_macs=2 ** 14, tiled_pack=tiled).bind()
+        assert plan.stats()["num_gemm"] > 0
+        plan.run(0, min(plan.d, 4))
+        vals.append(plan.result())
+        plan.close()
+    ref, _, _ = oracle.contract_sliced(tn, tree, ss.labels, slice_ids=range(0, min(ss.d, 4)))
+    for v in vals:
+        assert rel_err(v, ref) <= TOL
