@@ -247,6 +247,10 @@ __global__ void __launch_bounds__(256) pack_kernel(const PackParams p) {
     p.dst[e + p.plane_stride] = re - re_hi;
     p.dst[e + 2 * p.plane_stride] = im_hi;
     p.dst[e + 3 * p.plane_stride] = im - im_hi;
+    if (p.nplanes == 6) {
+      p.dst[e + 4 * p.plane_stride] = -im_hi;
+      p.dst[e + 5 * p.plane_stride] = im_hi - im;
+    }
   }
 }
 
@@ -298,6 +302,10 @@ __global__ void __launch_bounds__(256) perm_kernel(const PermParams p) {
         d[off + p.plane_stride] = v.x - re_hi;
         d[off + 2 * p.plane_stride] = im_hi;
         d[off + 3 * p.plane_stride] = v.y - im_hi;
+        if (p.mode == 2) {
+          d[off + 4 * p.plane_stride] = -im_hi;
+          d[off + 5 * p.plane_stride] = im_hi - v.y;
+        }
       }
     }
     __syncthreads();

@@ -111,6 +111,7 @@ struct Vertex {
   int64_t chunk = 0;
   int blk_apl = -1, blk_bpl = -1, blk_part = -1;
   int splits = 1;
+  bool swap = false;  // GEMM A operand taken from y (larger row count)
   int64_t tab_off = -1;  // element offset in the sum-table buffer
 };
 
@@ -481,9 +482,13 @@ int compile(Plan& P, const tnx_plan_desc* D) {
                       (double)v.macs >= P.gemm_min_macs;
     if (gemm) {
       v.kind = VK_GEMM;
+      // A takes the operand with more rows (output rows = A rows)
+      v.swap = v.N > v.M;
       z.labels = v.bl;
-      z.labels.insert(z.labels.end(), v.ml.begin(), v.ml.end());
-      z.labels.insert(z.labels.end(), v.nl.begin(), v.nl.end());
+      const std::vector<int>& first = v.swap ? v.nl : v.ml;
+      const std::vector<int>& second = v.swap ? v.ml : v.nl;
+      z.labels.insert(z.labels.end(), first.begin(), first.end());
+      z.labels.insert(z.labels.end(), second.begin(), second.end());
       v.kp = align_up(v.K, 16);
     } else {
       for (int l : x.labels)
@@ -518,9 +523,10 @@ int compile(Plan& P, const tnx_plan_desc* D) {
       z.block = add_block(ph, z.size * 8, st, last);
     }
     if (v.kind == VK_GEMM) {
-      v.blk_apl = add_block(ph, 16 * v.B * v.M * v.kp, st, st);
-      v.blk_bpl = add_block(ph, 16 * v.B * v.N * v.kp, st, st);
-      v.splits = ((v.B * v.M * v.N) % 2 == 0) ? gemm_choose_splits(v.B, v.M, v.N, v.kp) : 1;
+      const int64_t ra = v.swap ? v.N : v.M, rb = v.swap ? v.M : v.N;
+      v.blk_apl = add_block(ph, 16 * v.B * ra * v.kp, st, st);
+      v.blk_bpl = add_block(ph, 16 * v.B * rb * v.kp, st, st);
+      v.splits = ((v.B * v.M * v.N) % 2 == 0) ? gemm_choose_splits(v.B, ra, rb, v.kp) : 1;
       if (v.splits > 1) v.blk_part = add_block(ph, 8 * (int64_t)v.splits * v.B * v.M * v.N, st, st);
     }
   }
@@ -666,11 +672,15 @@ int lower(Plan& P) {
         rows_a.insert(rows_a.end(), v.ml.begin(), v.ml.end());
         std::vector<int> rows_b = v.bl;
         rows_b.insert(rows_b.end(), v.nl.begin(), v.nl.end());
+        if (v.swap) std::swap(rows_a, rows_b);
+        const TensorLoc& opa = v.swap ? y : x;
+        const TensorLoc& opb = v.swap ? x : y;
+        const int64_t ra = v.swap ? v.N : v.M, rb = v.swap ? v.M : v.N;
         for (int side = 0; side < 2; ++side) {
-          const TensorLoc& src = side == 0 ? x : y;
+          const TensorLoc& src = side == 0 ? opa : opb;
           const std::vector<int>& rows = side == 0 ? rows_a : rows_b;
           float* planes = side == 0 ? apl : bpl;
-          const int64_t nrows = side == 0 ? v.B * v.M : v.B * v.N;
+          const int64_t nrows = v.B * (side == 0 ? ra : rb);
           bool done = false;
           if (v.kp == v.K && !(P.flags & TNX_FLAG_NO_TILED_PACK)) {
             std::vector<int> dst = rows;
@@ -700,13 +710,14 @@ int lower(Plan& P) {
             pk.K = v.K;
             pk.kp = v.kp;
             pk.plane_stride = nrows * v.kp;
+            pk.nplanes = 4;
             P.packs.push_back(pk);
             out.push_back({L_PACK, (int)P.packs.size() - 1, v.ssa});
           }
         }
         GemmPlan g;
         float2* part = v.splits > 1 ? reinterpret_cast<float2*>(P.block_ptr(phase, v.blk_part)) : nullptr;
-        if (gemm_prepare(&g, apl, bpl, P.ptr(z), v.B, v.M, v.N, v.kp, v.splits, part, ebuf, sizeof(ebuf)))
+        if (gemm_prepare(&g, apl, bpl, P.ptr(z), v.B, ra, rb, v.kp, v.splits, part, ebuf, sizeof(ebuf)))
           return fail(TNX_ERR_CUDA, std::string("vertex ") + std::to_string(v.ssa) + ": " + ebuf);
         P.gemms.push_back(g);
         out.push_back({L_GEMM, (int)P.gemms.size() - 1, v.ssa});
@@ -1130,6 +1141,7 @@ int tnx_gemm_c64(const void* A, const void* B, void* C, int64_t batch, int64_t M
   pa.K = K;
   pa.kp = kp;
   pa.plane_stride = pa.rows * kp;
+  pa.nplanes = 4;
   simple(pb.row, batch * N, K);
   simple(pb.col, K, 1);
   pb.src = static_cast<const float2*>(B);
@@ -1138,6 +1150,7 @@ int tnx_gemm_c64(const void* A, const void* B, void* C, int64_t batch, int64_t M
   pb.K = K;
   pb.kp = kp;
   pb.plane_stride = pb.rows * kp;
+  pb.nplanes = 4;
   cudaError_t e = launch_pack(pa, st);
   if (e == cudaSuccess) e = launch_pack(pb, st);
   if (e != cudaSuccess) return fail(TNX_ERR_CUDA, cudaGetErrorString(e));

@@ -39,8 +39,9 @@ struct SimtParams {
   int32_t mode;
 };
 
-// Pack a complex64 tensor into four fp32 planes [re_hi, re_lo, im_hi, im_lo],
-// each [rows][kp] (rows = batch*R, K padded to kp with zeros); hi = tf32
+// Pack a complex64 tensor into fp32 planes [re_hi, re_lo, im_hi, im_lo]
+// (+ [-im_hi, -im_lo] when nplanes == 6, the GEMM B operand), each
+// [rows][kp] (rows = batch*R, K padded to kp with zeros); hi = tf32
 // truncation, lo = x - hi.
 struct PackParams {
   IdxMap row;             // row index -> src offset (st0)
@@ -51,6 +52,8 @@ struct PackParams {
   int64_t K;
   int64_t kp;
   int64_t plane_stride;   // rows * kp
+  int32_t nplanes;        // 4 or 6
+  int32_t pad;
 };
 
 // Shared-memory tiled permutation (K2).  The tile spans the innermost source
@@ -67,7 +70,7 @@ struct PermParams {
   int64_t plane_stride;   // mode 1: elements per plane
   int32_t ts;
   int32_t group;
-  int32_t mode;           // 0: complex64 copy, 1: split-TF32 planes
+  int32_t mode;           // 0: complex64 copy, 1: 4 split-TF32 planes, 2: 6 planes
   int32_t pad;
 };
 
@@ -118,7 +121,8 @@ struct GemmPlan {
   int32_t splits;         // split-K factor (1 = none)
   float2* partial;        // split-K workspace [splits][batch][M][N]
 };
-// Build tensor maps for planes laid out as [4][batch][M|N][kp] fp32.
+// Build tensor maps for planes laid out as [4][batch][M|N][kp] fp32; kp a
+// multiple of 16.
 int gemm_prepare(GemmPlan* g, const float* a_planes, const float* b_planes, float2* out,
                  int64_t batch, int64_t M, int64_t N, int64_t kp, int splits, float2* partial,
                  char* err, size_t errlen);
