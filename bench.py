@@ -250,11 +250,20 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TNX_BENCH_BACKEND=gloo lets the multi-rank logic be exercised with
+    # several ranks sharing one GPU (no kernel waits on another rank); the
+    # production path is NCCL with one GPU per rank.
+    backend = os.environ.get("TNX_BENCH_BACKEND", "nccl")
+    local = local % torch.cuda.device_count() if backend != "nccl" else local
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     from paper_2002_01935_b200.executor import SlicedPlan
+    from paper_2002_01935_b200.distributed import slice_range, allreduce_complex
     t_setup = time.perf_counter()
     tn, tree, ss, meta = workload(args)
     plan = SlicedPlan(tn, tree, ss, device=local, precision=args.precision)
@@ -269,11 +278,17 @@ def main():
     # ABI reads as "the library's own stream"
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    base = rank * (W + K)
+    # the job contracts the prefix [0, world*(W+K)) of the slice enumeration;
+    # each rank owns one contiguous block (bit-exact sub-range)
+    base, _ = slice_range(0, world * (W + K), world, rank)
+    red_dev = "cuda" if backend == "nccl" else "cpu"
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if backend == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
 
     # warm-up
     plan.run(base, base + W, stream)
@@ -294,17 +309,15 @@ def main():
     barrier()
     clocks = clk.stop()
     ms = e0.elapsed_time(e1)
-    t_max = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    t_max = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     ms_max = float(t_max.item())
 
     # final exchange: one all-reduce of the complex128 partial sums
     part = plan.result(stream)
-    flat = torch.from_numpy(np.ascontiguousarray(np.atleast_1d(part)).view(np.float64)).cuda()
     a0 = time.perf_counter()
-    if world > 1:
-        dist.all_reduce(flat, op=dist.ReduceOp.SUM)
+    total = allreduce_complex(part, device=red_dev)
     torch.cuda.synchronize()
     allreduce_ms = 1e3 * (time.perf_counter() - a0)
 
@@ -370,7 +383,7 @@ def main():
             plan.result(stream)
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
-        t_e = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        t_e = torch.tensor([e2e_s], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
         e2e_s = float(t_e.item())
@@ -416,7 +429,8 @@ def main():
                 "gpu_launches": K * st["launches_per_slice"],
                 "plan": {k: st[k] for k in ("num_gemm", "num_simt", "num_hoisted", "launches_per_slice",
                                             "work_arena_bytes")},
-                "allreduce_ms": allreduce_ms, "setup_s": setup_s}
+                "allreduce_ms": allreduce_ms, "setup_s": setup_s, "backend": backend if world > 1 else None,
+                "prefix_sum": [complex(np.asarray(total).ravel()[0]).real, complex(np.asarray(total).ravel()[0]).imag]}
         print(json.dumps(line, default=str))
     plan.close()
     if world > 1:
