@@ -19,6 +19,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <algorithm>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -449,6 +450,18 @@ int gemm_choose_splits(int64_t batch, int64_t M, int64_t N, int64_t kp) {
   return (int)std::max<int64_t>(1, s);
 }
 
+// k-blocks (of 16) accumulated in TMEM per promotion round; TNX_GEMM_PROMOTE
+// overrides (measured trade-off: accuracy vs TMEM-pipe load of the promotion).
+static int gemm_default_promote() {
+  static int v = 0;
+  if (!v) {
+    const char* e = getenv("TNX_GEMM_PROMOTE");
+    v = e ? atoi(e) : 4;
+    if (v < 1) v = 1;
+  }
+  return v;
+}
+
 cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
   GemmArgs a;
   a.out = g.out;
@@ -458,7 +471,7 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
   a.num_kb = (int32_t)(g.kp / BK);
   a.tiles_m = (int32_t)((g.M + BM - 1) / BM);
   a.tiles_n = (int32_t)((g.N + BN - 1) / BN);
-  a.promote = g.promote > 0 ? g.promote : 2;
+  a.promote = g.promote > 0 ? g.promote : gemm_default_promote();
   const int splits = g.splits > 1 ? g.splits : 1;
   a.kb_per_split = (a.num_kb + splits - 1) / splits;
   a.partial = splits > 1 ? g.partial : nullptr;
