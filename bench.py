@@ -339,14 +339,12 @@ def main():
             pack_bytes += 0  # accounted per operand below
     peaks, peak_kind = load_peaks()
     p_tf32 = measure_tf32_peak(torch) if not args.no_tf32_probe else None
+    # primary roofline: the driver-measured bf16 peak -> TF32 (half rate) -> /3 split passes
+    p_c = peaks["bf16_tflops"] / 2.0 / 3.0
+    peak_src = (f"{peak_kind} MEASURED_PEAKS bf16_tflops {peaks['bf16_tflops']} / 2 (TF32 = half the "
+                f"BF16 tensor rate) / 3 (split-TF32 passes)")
     if p_tf32:
-        p_c = p_tf32 / 3.0
-        peak_src = (f"live cuBLAS TF32 dense GEMM 8192^3 = {p_tf32:.1f} TFLOP/s (best of 5, same run) / 3 "
-                    f"split passes; bf16-derived alternative {peaks['bf16_tflops'] / 6.0:.1f} "
-                    f"({peak_kind} bf16_tflops {peaks['bf16_tflops']} / 2 / 3)")
-    else:
-        p_c = peaks["bf16_tflops"] / 2.0 / 3.0
-        peak_src = f"{peak_kind} bf16_tflops {peaks['bf16_tflops']} /2 (TF32) /3 (split passes)"
+        peak_src += f"; live cuBLAS TF32 8192^3 this run: {p_tf32:.1f} TFLOP/s (/3 = {p_tf32 / 3:.1f})"
     achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
     traffic = load_traffic()
     by_kind = {}

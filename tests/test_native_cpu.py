@@ -90,3 +90,26 @@ def test_vertex_kinds_and_hoisting():
     assert sum(v["macs"] for v in info) == plan.ops_per_slice
     assert plan.width == sliced_metrics(tree, tn, ss.labels)[0]
     plan.close()
+
+
+def test_accepts_reference_objects_when_available():
+    """The executor is a drop-in for the reference's own objects."""
+    import sys
+    ref = "/root/reference/pkg/src"
+    import os
+    if not os.path.isdir(ref):
+        pytest.skip("reference not present (GPU box)")
+    sys.path.insert(0, ref)
+    try:
+        from hypertn import network as rnet, tree as rtree
+        from hypertn.drivers import greedy as rgreedy
+    finally:
+        sys.path.remove(ref)
+    tn0 = gen.random_regular(16, 3, seed=2)
+    rtn = rnet.TensorNetwork([rnet.TensorNode(n.id, n.indices, n.data) for n in tn0.nodes],
+                             dict(tn0.index_table), ())
+    rt = rgreedy.greedy_sample(rtn, 1.0, 0.0, 0)
+    plan = SlicedPlan(rtn, rt, list(rtn.index_table)[:2])
+    assert plan.ops_per_slice * plan.d == sliced_metrics(rt, rtn, list(rtn.index_table)[:2])[1]
+    assert plan.ops_per_slice * 1 <= rtree.metrics(rt, rtn).cost * 4
+    plan.close()
