@@ -345,6 +345,257 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// 2-CTA variant (cta_group::2): a cluster of two CTAs on one TPC computes a
+// 256 x 128 complex tile.  Each CTA stages its own 128 A rows and half of the
+// B tile (64 rows) per plane; the leader CTA issues M=256 MMAs that read A
+// from both CTAs and exchange the B halves, so per-SM shared-memory operand
+// traffic per MMA drops from 8 KB to 6 KB.  TMA loads of both CTAs complete
+// on the leader's "full" barrier (peer bit cleared), MMA commits multicast to
+// both CTAs' "empty" / "tmem full" barriers, and both CTAs' epilogue warps
+// release a TMEM accumulator set by arriving on the leader's barrier.
+constexpr int BN_HALF = BN / 2;
+constexpr int A2_BYTES = BM * BK * 4;         // 8 KB per A plane (128 rows)
+constexpr int B2_BYTES = BN_HALF * BK * 4;    // 4 KB per B plane (64 rows)
+constexpr int STAGE2_BYTES = 4 * A2_BYTES + 4 * B2_BYTES;   // 48 KB
+constexpr int STAGES2 = 4;
+constexpr int SMEM2_BYTES = STAGES2 * STAGE2_BYTES + 1024 + 256;
+constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_2sm(uint32_t dst, const void* tmap, uint32_t mbar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(mbar & PEER_MASK), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void umma_tf32_2sm(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_2sm(uint32_t mbar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(mbar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint32_t local_addr) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(0));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+// M=256 (pair), N=128, D=f32, A=B=tf32 K-major.
+__host__ __device__ constexpr uint32_t idesc_tf32_2sm(bool neg_a) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((neg_a ? 1u : 0u) << 13) |
+         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    gemm_c64_3xtf32_2sm_kernel(const __grid_constant__ CUtensorMap tm_a,
+                               const __grid_constant__ CUtensorMap tm_b, const GemmArgs g) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES);
+  uint64_t* tfull = bars + 2 * STAGES2;
+  uint64_t* tempty = bars + 2 * STAGES2 + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES2 + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+
+  // pair tile (grouped rasterisation over 256-row pair tiles)
+  const int tile = blockIdx.x >> 1;
+  const int group_span = GROUP_M * g.tiles_n;
+  const int group = tile / group_span;
+  const int first_m = group * GROUP_M;
+  const int gm = min(g.tiles_m - first_m, GROUP_M);
+  const int tm = first_m + (tile % group_span) % gm;  // 256-row pair tile index
+  const int tn = (tile % group_span) / gm;
+  const int b = blockIdx.y;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_addr(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(smem_addr(&bars[s]), 1);
+      mbar_init(smem_addr(&bars[STAGES2 + s]), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(smem_addr(&tfull[s]), 1);
+      mbar_init(smem_addr(&tempty[s]), 16);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int kb_begin = blockIdx.z * g.kb_per_split;
+  const int nkb = min(g.num_kb - kb_begin, g.kb_per_split);
+  const int P = g.promote;
+  const int rounds = (nkb + P - 1) / P;
+  float2* const out = g.partial ? g.partial + (int64_t)blockIdx.z * g.batch * g.M * g.N : g.out;
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs) ----------------
+      const int row_a = (int)(b * g.M + (int64_t)tm * 256 + rank * 128);
+      const int row_b = (int)(b * g.N + (int64_t)tn * BN + rank * BN_HALF);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(smem_addr(&bars[STAGES2 + stage]), phase ^ 1u);
+        const uint32_t full = smem_addr(&bars[stage]);
+        if (leader) mbar_expect_tx(full, 2 * STAGE2_BYTES);
+        unsigned char* sbase = smem + stage * STAGE2_BYTES;
+        const int kc = (kb_begin + kb) * BK;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          tma_load_2d_2sm(smem_addr(sbase + p * A2_BYTES), &tm_a, full, kc, (int)(p * g.rows_a + row_a));
+          tma_load_2d_2sm(smem_addr(sbase + 4 * A2_BYTES + p * B2_BYTES), &tm_b, full, kc,
+                          (int)(p * g.rows_b + row_b));
+        }
+        if (++stage == STAGES2) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ---------------- MMA issuer (leader CTA) ----------------
+      constexpr uint32_t ID_POS = idesc_tf32_2sm(false);
+      constexpr uint32_t ID_NEG = idesc_tf32_2sm(true);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int r = 0; r < rounds; ++r) {
+        const int set = r & 1;
+        mbar_wait(smem_addr(&tempty[set]), ((uint32_t)(r >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t d_re = tmem_base + set * 256;
+        const uint32_t d_im = d_re + BN;
+        const int kb0 = r * P;
+        const int kb1 = min(nkb, kb0 + P);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(smem_addr(&bars[stage]), phase);
+          tc_fence_after();
+          const uint32_t sb = smem_addr(smem + stage * STAGE2_BYTES);
+#pragma unroll
+          for (int ks = 0; ks < BK / 8; ++ks) {
+            const uint32_t koff = ks * 32;
+            const uint64_t ar_h = umma_desc_sw64(sb + 0 * A2_BYTES + koff);
+            const uint64_t ar_l = umma_desc_sw64(sb + 1 * A2_BYTES + koff);
+            const uint64_t ai_h = umma_desc_sw64(sb + 2 * A2_BYTES + koff);
+            const uint64_t ai_l = umma_desc_sw64(sb + 3 * A2_BYTES + koff);
+            const uint32_t bb = sb + 4 * A2_BYTES + koff;
+            const uint64_t br_h = umma_desc_sw64(bb + 0 * B2_BYTES);
+            const uint64_t br_l = umma_desc_sw64(bb + 1 * B2_BYTES);
+            const uint64_t bi_h = umma_desc_sw64(bb + 2 * B2_BYTES);
+            const uint64_t bi_l = umma_desc_sw64(bb + 3 * B2_BYTES);
+            const uint32_t acc0 = (kb > kb0 || ks > 0) ? 1u : 0u;
+            umma_tf32_2sm(d_re, ar_h, br_l, ID_POS, acc0);
+            umma_tf32_2sm(d_re, ar_l, br_h, ID_POS, 1u);
+            umma_tf32_2sm(d_re, ai_h, bi_l, ID_NEG, 1u);
+            umma_tf32_2sm(d_re, ai_l, bi_h, ID_NEG, 1u);
+            umma_tf32_2sm(d_re, ar_h, br_h, ID_POS, 1u);
+            umma_tf32_2sm(d_re, ai_h, bi_h, ID_NEG, 1u);
+            umma_tf32_2sm(d_im, ar_h, bi_l, ID_POS, acc0);
+            umma_tf32_2sm(d_im, ar_l, bi_h, ID_POS, 1u);
+            umma_tf32_2sm(d_im, ai_h, br_l, ID_POS, 1u);
+            umma_tf32_2sm(d_im, ai_l, br_h, ID_POS, 1u);
+            umma_tf32_2sm(d_im, ar_h, bi_h, ID_POS, 1u);
+            umma_tf32_2sm(d_im, ai_h, br_h, ID_POS, 1u);
+          }
+          umma_commit_2sm(smem_addr(&bars[STAGES2 + stage]));
+          if (++stage == STAGES2) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        umma_commit_2sm(smem_addr(&tfull[set]));
+      }
+    }
+  } else {
+    // ---------------- promotion + epilogue (8 warps per CTA) ----------------
+    const int q = warp & 3;
+    const int h = (warp - 2) >> 2;
+    float mre[64], mim[64];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) {
+      mre[j] = 0.f;
+      mim[j] = 0.f;
+    }
+    const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16) + h * 64;
+    for (int r = 0; r < rounds; ++r) {
+      const int set = r & 1;
+      mbar_wait(smem_addr(&tfull[set]), (uint32_t)(r >> 1) & 1u);
+      tc_fence_after();
+      const uint32_t t0 = lane_base + set * 256;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t re[16], im[16];
+        tmem_ld16(t0 + j * 16, re);
+        tmem_ld16(t0 + BN + j * 16, im);
+        tmem_wait_ld();
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          mre[j * 16 + t] += __uint_as_float(re[t]);
+          mim[j * 16 + t] += __uint_as_float(im[t]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(smem_addr(&tempty[set]));
+    }
+    const int64_t row = (int64_t)tm * 256 + rank * 128 + q * 32 + lane;
+    if (row < g.M) {
+      float2* orow = out + ((int64_t)b * g.M + row) * g.N;
+      const int64_t col0 = (int64_t)tn * BN + h * 64;
+      if (col0 + 64 <= g.N && (g.N & 1) == 0) {
+        float4* dst = reinterpret_cast<float4*>(orow + col0);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          dst[j] = make_float4(mre[2 * j], mim[2 * j], mre[2 * j + 1], mim[2 * j + 1]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 64; ++j)
+          if (col0 + j < g.N) orow[col0 + j] = make_float2(mre[j], mim[j]);
+      }
+    }
+  }
+  __syncwarp();
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -364,13 +615,13 @@ EncodeTiledFn get_encode(char* err, size_t errlen) {
   return fn;
 }
 
-int encode_planes(void* tmap, const float* base, int64_t rows_total, int64_t kp, char* err,
-                  size_t errlen) {
+int encode_planes(void* tmap, const float* base, int64_t rows_total, int64_t kp, int box_rows,
+                  char* err, size_t errlen) {
   EncodeTiledFn enc = get_encode(err, errlen);
   if (!enc) return 1;
   cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows_total};
   cuuint64_t strides[1] = {(cuuint64_t)(kp * 4)};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)BM};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(reinterpret_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                    const_cast<float*>(base), dims, strides, box, estr,
@@ -386,9 +637,25 @@ int encode_planes(void* tmap, const float* base, int64_t rows_total, int64_t kp,
 
 }  // namespace
 
+// 2-CTA pairs for tall GEMMs with enough pair tiles (TNX_GEMM_2SM=0 disables).
+int gemm_use_2sm(int64_t batch, int64_t M, int64_t N, int64_t kp) {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("TNX_GEMM_2SM");
+    mode = e ? atoi(e) : 1;
+  }
+  if (!mode) return 0;
+  (void)kp;
+  const int64_t pair_tiles = ((M + 255) / 256) * ((N + BN - 1) / BN) * batch;
+  return M >= 256 && pair_tiles >= 74 ? 1 : 0;
+}
+
 int gemm_init_attributes(char* err, size_t errlen) {
-  cudaError_t e = cudaFuncSetAttribute(gemm_c64_3xtf32_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  cudaError_t e = cudaFuncSetAttribute(gemm_c64_3xtf32_2sm_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(gemm_c64_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             SMEM_BYTES);
   if (e != cudaSuccess) {
     snprintf(err, errlen, "cudaFuncSetAttribute(gemm): %s", cudaGetErrorString(e));
     return 1;
@@ -414,8 +681,10 @@ int gemm_prepare(GemmPlan* g, const float* a_planes, const float* b_planes, floa
     snprintf(err, errlen, "gemm: row coordinate exceeds int32");
     return 1;
   }
-  if (encode_planes(g->tmap_a, a_planes, 4 * batch * M, kp, err, errlen)) return 1;
-  if (encode_planes(g->tmap_b, b_planes, 4 * batch * N, kp, err, errlen)) return 1;
+  g->two_sm = gemm_use_2sm(batch, M, N, kp);
+  if (encode_planes(g->tmap_a, a_planes, 4 * batch * M, kp, BM, err, errlen)) return 1;
+  if (encode_planes(g->tmap_b, b_planes, 4 * batch * N, kp, g->two_sm ? BN_HALF : BN, err, errlen))
+    return 1;
   g->out = out;
   g->M = M;
   g->N = N;
@@ -478,10 +747,28 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
   a.rows_a = g.batch * g.M;
   a.rows_b = g.batch * g.N;
   const int zs = (a.num_kb + a.kb_per_split - 1) / a.kb_per_split;
-  dim3 grid((unsigned)(a.tiles_m * a.tiles_n), (unsigned)g.batch, (unsigned)zs);
   const CUtensorMap* ta = reinterpret_cast<const CUtensorMap*>(g.tmap_a);
   const CUtensorMap* tb = reinterpret_cast<const CUtensorMap*>(g.tmap_b);
-  gemm_c64_3xtf32_kernel<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(*ta, *tb, a);
+  if (g.two_sm) {
+    a.tiles_m = (int32_t)((g.M + 255) / 256);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * a.tiles_m * a.tiles_n), (unsigned)g.batch, (unsigned)zs);
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = SMEM2_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t le = cudaLaunchKernelEx(&cfg, gemm_c64_3xtf32_2sm_kernel, *ta, *tb, a);
+    if (le != cudaSuccess) return le;
+  } else {
+    dim3 grid((unsigned)(a.tiles_m * a.tiles_n), (unsigned)g.batch, (unsigned)zs);
+    gemm_c64_3xtf32_kernel<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(*ta, *tb, a);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || zs == 1) return e;
   const int64_t n = g.batch * g.M * g.N;  // complex elements

@@ -119,6 +119,7 @@ struct GemmPlan {
   int32_t ok;
   int32_t promote;        // k-blocks (of 16) per TMEM accumulation round
   int32_t splits;         // split-K factor (1 = none)
+  int32_t two_sm;         // 2-CTA (cta_group::2) variant
   float2* partial;        // split-K workspace [splits][batch][M][N]
 };
 // Build tensor maps for planes laid out as [4][batch][M|N][kp] fp32; kp a
@@ -127,6 +128,7 @@ int gemm_prepare(GemmPlan* g, const float* a_planes, const float* b_planes, floa
                  int64_t batch, int64_t M, int64_t N, int64_t kp, int splits, float2* partial,
                  char* err, size_t errlen);
 int gemm_choose_splits(int64_t batch, int64_t M, int64_t N, int64_t kp);
+int gemm_use_2sm(int64_t batch, int64_t M, int64_t N, int64_t kp);
 cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st);
 int gemm_init_attributes(char* err, size_t errlen);
 
