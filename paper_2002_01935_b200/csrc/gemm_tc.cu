@@ -4,8 +4,9 @@
 //
 //   C[b,m,n] = sum_k A[b,m,k] * B[b,n,k]          (complex64 in/out)
 //
-// Operands arrive as four fp32 planes each ([re_hi, re_lo, im_hi, im_lo],
-// [batch*rows][kp] K-major, written by the pack kernel).  Per 8-wide k-step
+// Operands arrive as four fp32 planes each ([re_hi, re_lo, im_hi, im_lo]),
+// K-blocked [plane][kp/16][batch*rows][16] so that every TMA box (3-D tensor
+// map) is one contiguous 8 KB block, written by the pack kernels.  Per 8-wide k-step
 // one elected thread issues 12 tcgen05.mma.kind::tf32 (M=128, N=128, K=8):
 //
 //   Cre += Ar_h Br_h + Ar_h Br_l + Ar_l Br_h - (Ai_h Bi_h + Ai_h Bi_l + Ai_l Bi_h)
@@ -71,6 +72,15 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, uint
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
       "[%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(mbar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* tmap, uint32_t mbar, int c0,
+                                            int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(mbar), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
 
@@ -218,13 +228,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t full = smem_addr(&bars[stage]);
         mbar_expect_tx(full, STAGE_BYTES);
         unsigned char* sbase = smem + stage * STAGE_BYTES;
-        const int kc = (kb_begin + kb) * BK;
+        const int kbg = kb_begin + kb;  // global k-block
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-          tma_load_2d(smem_addr(sbase + p * PLANE_BYTES), &tm_a, full, kc,
-                      (int)(p * g.rows_a + row_a));
-          tma_load_2d(smem_addr(sbase + (4 + p) * PLANE_BYTES), &tm_b, full, kc,
-                      (int)(p * g.rows_b + row_b));
+          tma_load_3d(smem_addr(sbase + p * PLANE_BYTES), &tm_a, full, 0, row_a, p * g.num_kb + kbg);
+          tma_load_3d(smem_addr(sbase + (4 + p) * PLANE_BYTES), &tm_b, full, 0, row_b,
+                      p * g.num_kb + kbg);
         }
         if (++stage == STAGES) {
           stage = 0;
@@ -370,11 +379,12 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void tma_load_2d_2sm(uint32_t dst, const void* tmap, uint32_t mbar, int c0, int c1) {
+__device__ __forceinline__ void tma_load_3d_2sm(uint32_t dst, const void* tmap, uint32_t mbar, int c0, int c1,
+                                                int c2) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(mbar & PEER_MASK), "r"(c0), "r"(c1)
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(mbar & PEER_MASK), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
 __device__ __forceinline__ void umma_tf32_2sm(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
@@ -470,12 +480,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t full = smem_addr(&bars[stage]);
         if (leader) mbar_expect_tx(full, 2 * STAGE2_BYTES);
         unsigned char* sbase = smem + stage * STAGE2_BYTES;
-        const int kc = (kb_begin + kb) * BK;
+        const int kbg = kb_begin + kb;  // global k-block
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-          tma_load_2d_2sm(smem_addr(sbase + p * A2_BYTES), &tm_a, full, kc, (int)(p * g.rows_a + row_a));
-          tma_load_2d_2sm(smem_addr(sbase + 4 * A2_BYTES + p * B2_BYTES), &tm_b, full, kc,
-                          (int)(p * g.rows_b + row_b));
+          tma_load_3d_2sm(smem_addr(sbase + p * A2_BYTES), &tm_a, full, 0, row_a, p * g.num_kb + kbg);
+          tma_load_3d_2sm(smem_addr(sbase + 4 * A2_BYTES + p * B2_BYTES), &tm_b, full, 0, row_b,
+                          p * g.num_kb + kbg);
         }
         if (++stage == STAGES2) {
           stage = 0;
@@ -619,11 +629,13 @@ int encode_planes(void* tmap, const float* base, int64_t rows_total, int64_t kp,
                   char* err, size_t errlen) {
   EncodeTiledFn enc = get_encode(err, errlen);
   if (!enc) return 1;
-  cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows_total};
-  cuuint64_t strides[1] = {(cuuint64_t)(kp * 4)};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(reinterpret_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+  // K-blocked planes [plane][kp/16][rows][16]: every box is one contiguous
+  // block of box_rows x 64 B (rows past `rows` are zero-filled).
+  cuuint64_t dims[3] = {(cuuint64_t)BK, (cuuint64_t)rows_total, (cuuint64_t)(4 * (kp / BK))};
+  cuuint64_t strides[2] = {(cuuint64_t)(BK * 4), (cuuint64_t)(rows_total * BK * 4)};
+  cuuint32_t box[3] = {(cuuint32_t)BK, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(reinterpret_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                    const_cast<float*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -682,8 +694,8 @@ int gemm_prepare(GemmPlan* g, const float* a_planes, const float* b_planes, floa
     return 1;
   }
   g->two_sm = gemm_use_2sm(batch, M, N, kp);
-  if (encode_planes(g->tmap_a, a_planes, 4 * batch * M, kp, BM, err, errlen)) return 1;
-  if (encode_planes(g->tmap_b, b_planes, 4 * batch * N, kp, g->two_sm ? BN_HALF : BN, err, errlen))
+  if (encode_planes(g->tmap_a, a_planes, batch * M, kp, BM, err, errlen)) return 1;
+  if (encode_planes(g->tmap_b, b_planes, batch * N, kp, g->two_sm ? BN_HALF : BN, err, errlen))
     return 1;
   g->out = out;
   g->M = M;

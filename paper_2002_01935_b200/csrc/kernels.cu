@@ -8,7 +8,8 @@
 //               thread-per-output, warp-per-output (lane-split sum, shuffle
 //               reduce) and split-reduction (block partials + finalize) modes.
 //  K2 pack    : permute a complex64 tensor into the four split-TF32 planes the
-//               tcgen05 GEMM consumes (coalesced along the padded K axis).
+//               tcgen05 GEMM consumes, K-blocked [kp/16][rows][16] (gather
+//               fallback; the tiled permute `perm_kernel` is the fast path).
 //  K6 accum   : root -> tn.output order, Kahan-compensated complex128
 //               accumulation across slices.
 #include <algorithm>
@@ -227,11 +228,15 @@ cudaError_t launch_simt(const SimtParams& p, cudaStream_t st) {
 
 // ------------------------------------------------------------------ pack
 __global__ void __launch_bounds__(256) pack_kernel(const PackParams p) {
+  // destination planes are K-blocked: offset(r, k) = ((k / 16) * rows + r) * 16 + k % 16
   const int64_t total = p.rows * p.kp;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
-    const int64_t r = e / p.kp;
-    const int64_t k = e - r * p.kp;
+    const int64_t ki = e & 15;
+    const int64_t q = e >> 4;
+    const int64_t kb = q / p.rows;
+    const int64_t r = q - kb * p.rows;
+    const int64_t k = kb * 16 + ki;
     float re = 0.f, im = 0.f;
     if (k < p.K) {
       int64_t off = 0;
@@ -247,10 +252,6 @@ __global__ void __launch_bounds__(256) pack_kernel(const PackParams p) {
     p.dst[e + p.plane_stride] = re - re_hi;
     p.dst[e + 2 * p.plane_stride] = im_hi;
     p.dst[e + 3 * p.plane_stride] = im - im_hi;
-    if (p.nplanes == 6) {
-      p.dst[e + 4 * p.plane_stride] = -im_hi;
-      p.dst[e + 5 * p.plane_stride] = im_hi - im;
-    }
   }
 }
 

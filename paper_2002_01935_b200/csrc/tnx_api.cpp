@@ -682,9 +682,21 @@ int lower(Plan& P) {
           float* planes = side == 0 ? apl : bpl;
           const int64_t nrows = v.B * (side == 0 ? ra : rb);
           bool done = false;
-          if (v.kp == v.K && !(P.flags & TNX_FLAG_NO_TILED_PACK)) {
-            std::vector<int> dst = rows;
-            dst.insert(dst.end(), v.cl.begin(), v.cl.end());
+          // K-blocked plane layout = row-major order [K outer][rows][K inner = 16]
+          std::vector<int> k_in, k_out;
+          {
+            int64_t pr = 1;
+            int i = (int)v.cl.size() - 1;
+            for (; i >= 0 && pr < 16; --i) pr *= P.dims[v.cl[i]];
+            if (pr == 16) {
+              k_out.assign(v.cl.begin(), v.cl.begin() + (i + 1));
+              k_in.assign(v.cl.begin() + (i + 1), v.cl.end());
+            }
+          }
+          if (v.kp == v.K && !k_in.empty() && !(P.flags & TNX_FLAG_NO_TILED_PACK)) {
+            std::vector<int> dst = k_out;
+            dst.insert(dst.end(), rows.begin(), rows.end());
+            dst.insert(dst.end(), k_in.begin(), k_in.end());
             PermParams pp;
             int64_t toff = 0;
             const size_t mark = P.ptabs.size();
