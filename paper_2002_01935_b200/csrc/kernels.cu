@@ -313,12 +313,72 @@ __global__ void __launch_bounds__(256) perm_kernel(const PermParams p) {
   }
 }
 
+// Vectorised variant: element pairs (t, t+1) are contiguous and 16 B / 8 B
+// aligned in source and destination, ts is a power of two.
+__global__ void __launch_bounds__(256) perm_vec_kernel(const PermParams p) {
+  extern __shared__ __align__(16) unsigned char perm_smem[];
+  __shared__ int64_t base_s[64], base_d[64];
+  const int ts = p.ts;
+  const int lg = p.ts_log2;
+  const int G = p.group;
+  int32_t* t_src = reinterpret_cast<int32_t*>(perm_smem);
+  int32_t* t_idx = t_src + ts;
+  int32_t* t_dst = t_idx + ts;
+  float2* tile = reinterpret_cast<float2*>(perm_smem + ((size_t)(3 * ts * 4 + 15) & ~(size_t)15));
+  for (int i = threadIdx.x; i < 3 * ts; i += blockDim.x) t_src[i] = p.tab[i];
+  const int64_t nchunks = (p.n_outer + G - 1) / G;
+  const int half_mask = (ts >> 1) - 1;
+  const int half_lg = lg - 1;
+  float* d = static_cast<float*>(p.dst);
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const int64_t o0 = c * G;
+    const int gcount = (int)(p.n_outer - o0 < (int64_t)G ? p.n_outer - o0 : (int64_t)G);
+    if (threadIdx.x < gcount) {
+      int64_t sb = 0, db = 0;
+      decode2(p.outer, o0 + threadIdx.x, sb, db);
+      base_s[threadIdx.x] = sb;
+      base_d[threadIdx.x] = db;
+    }
+    __syncthreads();
+    const int npairs = gcount << half_lg;
+    for (int e = threadIdx.x; e < npairs; e += blockDim.x) {
+      const int j = e >> half_lg, t = (e & half_mask) << 1;
+      const float4 v = *reinterpret_cast<const float4*>(p.src + base_s[j] + t_src[t]);
+      tile[(j << lg) + t_idx[t]] = make_float2(v.x, v.y);
+      tile[(j << lg) + t_idx[t + 1]] = make_float2(v.z, v.w);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < npairs; e += blockDim.x) {
+      const int j = e >> half_lg, t = (e & half_mask) << 1;
+      const float2 a = tile[(j << lg) + t];
+      const float2 b = tile[(j << lg) + t + 1];
+      const int64_t off = base_d[j] + t_dst[t];
+      if (p.mode == 0) {
+        *reinterpret_cast<float4*>(static_cast<float2*>(p.dst) + off) = make_float4(a.x, a.y, b.x, b.y);
+      } else {
+        const float ar = __uint_as_float(__float_as_uint(a.x) & 0xffffe000u);
+        const float ai = __uint_as_float(__float_as_uint(a.y) & 0xffffe000u);
+        const float br = __uint_as_float(__float_as_uint(b.x) & 0xffffe000u);
+        const float bi = __uint_as_float(__float_as_uint(b.y) & 0xffffe000u);
+        *reinterpret_cast<float2*>(d + off) = make_float2(ar, br);
+        *reinterpret_cast<float2*>(d + off + p.plane_stride) = make_float2(a.x - ar, b.x - br);
+        *reinterpret_cast<float2*>(d + off + 2 * p.plane_stride) = make_float2(ai, bi);
+        *reinterpret_cast<float2*>(d + off + 3 * p.plane_stride) = make_float2(a.y - ai, b.y - bi);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 cudaError_t launch_perm(const PermParams& p, cudaStream_t st) {
   const size_t smem = (((size_t)3 * p.ts * 4 + 15) & ~(size_t)15) + (size_t)p.ts * p.group * 8;
   const int64_t nchunks = (p.n_outer + p.group - 1) / p.group;
   int blocks = (int)std::min<int64_t>(nchunks, 148 * 8);
   if (blocks < 1) blocks = 1;
-  perm_kernel<<<blocks, 256, smem, st>>>(p);
+  if (p.vec)
+    perm_vec_kernel<<<blocks, 256, smem, st>>>(p);
+  else
+    perm_kernel<<<blocks, 256, smem, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -612,6 +612,22 @@ bool build_perm(Plan& P, const TensorLoc& t, const std::vector<int>& dst, int mo
   pp.ts = (int32_t)ts;
   pp.group = (int32_t)std::max<int64_t>(1, std::min<int64_t>(64, 2048 / ts));
   pp.mode = mode;
+  pp.ts_log2 = -1;
+  if ((ts & (ts - 1)) == 0) {
+    int lg = 0;
+    while ((int64_t(1) << lg) < ts) ++lg;
+    pp.ts_log2 = lg;
+  }
+  // vectorised path: pairs (t, t+1) contiguous and even-aligned on both sides,
+  // outer strides even (so every base keeps the alignment)
+  bool vec = pp.ts_log2 >= 1;
+  for (int64_t e = 0; vec && e < ts; e += 2) {
+    if (T_src[e + 1] != T_src[e] + 1 || (T_src[e] & 1)) vec = false;
+    if (T_dst[e + 1] != T_dst[e] + 1 || (T_dst[e] & 1)) vec = false;
+  }
+  for (int i = 0; vec && i < pp.outer.n; ++i)
+    if ((pp.outer.st0[i] & 1) || (pp.outer.st1[i] & 1)) vec = false;
+  pp.vec = vec ? 1 : 0;
   return true;
 }
 
@@ -704,6 +720,7 @@ int lower(Plan& P) {
               pp.src = P.ptr(src);
               pp.dst = planes;
               pp.plane_stride = nrows * v.kp;
+              if ((pp.plane_stride & 1) || (src.arena == AR_POOL && (src.offset & 1))) pp.vec = 0;
               pp.tab = reinterpret_cast<const int32_t*>(toff);  // rebased after upload
               P.perms.push_back(pp);
               out.push_back({L_PERM, (int)P.perms.size() - 1, v.ssa});

@@ -70,7 +70,9 @@ struct PermParams {
   int64_t plane_stride;   // mode 1: elements per plane
   int32_t ts;
   int32_t group;
-  int32_t mode;           // 0: complex64 copy, 1: 4 split-TF32 planes, 2: 6 planes
+  int32_t mode;           // 0: complex64 copy, 1: 4 split-TF32 planes
+  int32_t vec;            // 1: element pairs contiguous + aligned on both sides
+  int32_t ts_log2;        // log2(ts) if ts is a power of two, else -1
   int32_t pad;
 };
 
