@@ -349,13 +349,14 @@ def sycamore_circuit(m, seed=0, bitstring=None, simplify=True):
     qs = _sycamore_layout()
     pos = {q: i for i, q in enumerate(qs)}
     nq = len(qs)
+    # A/B: couplers along one lattice diagonal (even / odd rows), C/D: the
+    # other diagonal -- each pattern is a matching; ABCDCDAB cycling
     groups = {"A": [], "B": [], "C": [], "D": []}
     for (r, c), i in pos.items():
-        for dr, dc, g in ((1, 1, "A"), (1, -1, "B")):
-            nb = (r + dr, c + dc)
+        for dc, even, odd in ((1, "A", "B"), (-1, "C", "D")):
+            nb = (r + 1, c + dc)
             if nb in pos:
-                key = g if r % 2 == 0 else ("C" if g == "A" else "D")
-                groups[key].append((i, pos[nb]))
+                groups[even if r % 2 == 0 else odd].append((i, pos[nb]))
     order = "ABCDCDAB"
     circ = _CircuitTN(nq)
     last = [None] * nq

@@ -1,0 +1,58 @@
+"""Parity of the five BASELINE.json configurations (reference-driver trees,
+greedy_slice slice sets) at slice widths the CPU oracle finishes in seconds.
+Tolerance: |c_gpu - c_ref| <= 1e-5 |c_ref| + 1e-6 ||x_root|| ||y_root||
+(the second term only matters for slices that are zero or nearly zero in
+exact arithmetic, common in sliced circuits)."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2002_01935_b200.executor import SlicedPlan
+from paper_2002_01935_b200.harness.workloads import load_workload
+from paper_2002_01935_b200.slicing import slice_assignment
+
+pytestmark = pytest.mark.gpu
+
+CASES = [("cfg1_3reg50", None), ("cfg2_5reg100", 24), ("cfg3_lattice20", None),
+         ("cfg3_lattice20", 21), ("cfg4_7x7_d40", 24), ("cfg5_syc53_m12", 24)]
+
+
+def _root_check(tn, tree, ss, plan, s):
+    rec = {}
+    keep = {tree.root, *tree.children(tree.root)}
+
+    class R(dict):
+        def __setitem__(self, k, v):
+            if k in keep:
+                dict.__setitem__(self, k, v)
+    rec = R()
+    ref, _, ops, _ = oracle.contract_one(tn, tree, ss.labels, slice_assignment(tn, ss, s), record=rec)
+    a, b = tree.children(tree.root)
+    scale = np.linalg.norm(rec[a][1].ravel()) * np.linalg.norm(rec[b][1].ravel())
+    plan.reset()
+    plan.run(s, s + 1)
+    got = plan.result()
+    err = np.linalg.norm(np.ravel(got - ref))
+    assert err <= 1e-5 * np.linalg.norm(np.ravel(ref)) + 1e-6 * scale, (s, got, ref, scale)
+    assert ops == plan.ops_per_slice
+    return ref
+
+
+@pytest.mark.parametrize("name,ws", CASES, ids=[f"{n}-ws{w}" for n, w in CASES])
+def test_config_slices(name, ws):
+    tn, tree, ss, meta = load_workload(name, ws=ws)
+    plan = SlicedPlan(tn, tree, ss).bind()
+    try:
+        st = plan.stats()
+        assert st["num_gemm"] > 0 or name == "cfg1_3reg50"
+        ids = sorted({0, plan.d - 1, int(np.random.default_rng(0).integers(plan.d))})
+        for s in ids[:3]:
+            _root_check(tn, tree, ss, plan, s)
+        if plan.d == 1:
+            # full value must also match the unsliced oracle at 1e-5 relative
+            full, _, _ = oracle.contract(tn, tree)
+            plan.reset()
+            plan.run()
+            assert abs(complex(plan.result()) - full) <= 1e-5 * abs(full)
+    finally:
+        plan.close()
