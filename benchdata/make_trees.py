@@ -33,6 +33,8 @@ CONFIGS = {
     "cfg2_5reg100": (lambda: gen.random_regular(100, 5, seed=0), 48, False),
     "cfg3_lattice20": (lambda: gen.square_lattice(20, seed=0), 24, True),
     "cfg4_7x7_d40": (lambda: gen.grid_circuit(7, 7, 40, seed=0), 48, False),
+    "cfg4p_7x7_d16": (lambda: gen.grid_circuit(7, 7, 16, seed=0), 48, True),
+    "cfg4p_7x7_d20": (lambda: gen.grid_circuit(7, 7, 20, seed=0), 48, True),
     "cfg5_syc53_m12": (lambda: gen.sycamore_circuit(12, seed=0), 48, False),
 }
 

@@ -29,6 +29,12 @@ CONFIGS = {
                            desc="20x20 OBC square lattice, bond dim 2, scalar"),
     "cfg4_7x7_d40": dict(make=lambda: gen.grid_circuit(7, 7, 40, seed=0), ws=27,
                          desc="rectangular 7x7 (1+40+1) random circuit amplitude, 742 rank-3 tensors"),
+    # parity-only companions of cfg4 (same generator, shallower): the full
+    # amplitude is computable by the CPU oracle
+    "cfg4p_7x7_d16": dict(make=lambda: gen.grid_circuit(7, 7, 16, seed=0), ws=16,
+                          desc="7x7 (1+16+1) circuit amplitude (parity companion of cfg4)"),
+    "cfg4p_7x7_d20": dict(make=lambda: gen.grid_circuit(7, 7, 20, seed=0), ws=21,
+                          desc="7x7 (1+20+1) circuit amplitude (parity companion of cfg4)"),
     "cfg5_syc53_m12": dict(make=lambda: gen.sycamore_circuit(12, seed=0), ws=27,
                            desc="Sycamore-like 53-qubit m=12 circuit amplitude, synthetic fSim"),
 }
