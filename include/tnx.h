@@ -56,7 +56,9 @@ enum { TNX_LOC_HOST = 0, TNX_LOC_DEVICE = 1 };
 enum {
   TNX_FLAG_NO_GRAPH = 1u << 0,   /* launch per-slice steps directly (debug) */
   TNX_FLAG_NO_HOIST = 1u << 1,   /* recompute slice-invariant subtrees per slice */
-  TNX_FLAG_NO_TILED_PACK = 1u << 2  /* GEMM operands via the gather pack kernel only */
+  TNX_FLAG_NO_TILED_PACK = 1u << 2, /* GEMM operands via the gather pack kernel only */
+  TNX_FLAG_NO_DIRECT = 1u << 3      /* no GEMM->GEMM operand-plane fusion (every
+                                       intermediate materialised; debug dumps) */
 };
 
 /*

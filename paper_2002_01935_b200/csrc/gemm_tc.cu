@@ -145,10 +145,83 @@ struct GemmArgs {
   int32_t num_kb;        // kp / BK
   int32_t tiles_m, tiles_n;
   int32_t promote;       // k-blocks accumulated in TMEM before promotion
+  int32_t group_m;       // rasterisation: M tiles per group
   int32_t kb_per_split;  // split-K: k-blocks per CTA along grid.z
   float2* partial;       // split-K workspace [splits][batch][M][N] (nullptr: 1 split)
   int64_t rows_a, rows_b;  // batch * M, batch * N (rows per plane)
+  int32_t direct;        // 1: store as the parent's split-TF32 planes
+  int32_t pad;
+  float* dplanes;
+  int64_t dplane_stride;
+  IdxMap fmap, gmap;
 };
+
+__device__ __forceinline__ int64_t map_offset(const IdxMap& m, int64_t idx) {
+  int64_t o = 0;
+#pragma unroll 1
+  for (int i = m.n - 1; i >= 0; --i) {
+    int64_t r;
+    if (m.lg[i] >= 0) {
+      r = idx & (m.dim[i] - 1);
+      idx >>= m.lg[i];
+    } else {
+      const int64_t q = idx / m.dim[i];
+      r = idx - q * m.dim[i];
+      idx = q;
+    }
+    o += r * m.st0[i];
+  }
+  return o;
+}
+
+// Epilogue store of one thread's 64 promoted columns of row `row` (global
+// row index b*M + m).  Plain mode: interleaved complex64.  Direct mode: the
+// four split-TF32 planes of the parent GEMM operand, column offsets from the
+// per-CTA table `gtab` (built by the epilogue warps once the main loop is
+// done and the pipeline's shared memory is free).
+__device__ __forceinline__ void epilogue_store(const GemmArgs& g, float2* out, int64_t grow,
+                                               bool row_ok, int64_t col0, int hcol,
+                                               const float (&mre)[64], const float (&mim)[64],
+                                               const int64_t* gtab) {
+  if (!row_ok) return;
+  if (g.direct) {
+    const int64_t f = map_offset(g.fmap, grow);
+    float* d = g.dplanes;
+    const int64_t ps = g.dplane_stride;
+#pragma unroll
+    for (int j = 0; j < 64; ++j) {
+      if (col0 + j >= g.N) continue;
+      const int64_t off = f + gtab[hcol + j];
+      const float re = mre[j], im = mim[j];
+      const float rh = __uint_as_float(__float_as_uint(re) & 0xffffe000u);
+      const float ih = __uint_as_float(__float_as_uint(im) & 0xffffe000u);
+      d[off] = rh;
+      d[off + ps] = re - rh;
+      d[off + 2 * ps] = ih;
+      d[off + 3 * ps] = im - ih;
+    }
+    return;
+  }
+  float2* orow = out + grow * g.N;
+  if (col0 + 64 <= g.N && (g.N & 1) == 0) {
+    float4* dst = reinterpret_cast<float4*>(orow + col0);
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      dst[j] = make_float4(mre[2 * j], mim[2 * j], mre[2 * j + 1], mim[2 * j + 1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 64; ++j)
+      if (col0 + j < g.N) orow[col0 + j] = make_float2(mre[j], mim[j]);
+  }
+}
+
+// Column-offset table of this CTA's 128 output columns (direct mode); called
+// by all 256 epilogue threads after the last accumulator round.
+__device__ __forceinline__ void build_gtab(const GemmArgs& g, int64_t* gtab, int64_t col_base) {
+  const int e = threadIdx.x - 64;
+  if (e < BN) gtab[e] = (col_base + e < g.N) ? map_offset(g.gmap, col_base + e) : 0;
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+}
 
 __device__ __forceinline__ void mbar_arrive(uint32_t a) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
@@ -179,10 +252,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   // grouped rasterisation of the (m, n) tile grid for L2 reuse
   const int tile = blockIdx.x;
-  const int group_span = GROUP_M * g.tiles_n;
+  const int group_span = g.group_m * g.tiles_n;
   const int group = tile / group_span;
-  const int first_m = group * GROUP_M;
-  const int gm = min(g.tiles_m - first_m, GROUP_M);
+  const int first_m = group * g.group_m;
+  const int gm = min(g.tiles_m - first_m, g.group_m);
   const int tm = first_m + (tile % group_span) % gm;
   const int tn = (tile % group_span) / gm;
   const int b = blockIdx.y;
@@ -328,20 +401,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (lane == 0) mbar_arrive(smem_addr(&tempty[set]));
     }
     const int64_t row = (int64_t)tm * BM + q * 32 + lane;
-    if (row < g.M) {
-      float2* orow = out + ((int64_t)b * g.M + row) * g.N;
-      const int64_t col0 = (int64_t)tn * BN + h * 64;
-      if (col0 + 64 <= g.N && (g.N & 1) == 0) {
-        float4* dst = reinterpret_cast<float4*>(orow + col0);
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          dst[j] = make_float4(mre[2 * j], mim[2 * j], mre[2 * j + 1], mim[2 * j + 1]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 64; ++j)
-          if (col0 + j < g.N) orow[col0 + j] = make_float2(mre[j], mim[j]);
-      }
-    }
+    int64_t* gtab = reinterpret_cast<int64_t*>(smem);  // pipeline smem is free now
+    if (g.direct) build_gtab(g, gtab, (int64_t)tn * BN);
+    epilogue_store(g, out, (int64_t)b * g.M + row, row < g.M, (int64_t)tn * BN + h * 64, h * 64, mre,
+                   mim, gtab);
   }
   __syncwarp();
   tc_fence_before();
@@ -431,10 +494,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   // pair tile (grouped rasterisation over 256-row pair tiles)
   const int tile = blockIdx.x >> 1;
-  const int group_span = GROUP_M * g.tiles_n;
+  const int group_span = g.group_m * g.tiles_n;
   const int group = tile / group_span;
-  const int first_m = group * GROUP_M;
-  const int gm = min(g.tiles_m - first_m, GROUP_M);
+  const int first_m = group * g.group_m;
+  const int gm = min(g.tiles_m - first_m, g.group_m);
   const int tm = first_m + (tile % group_span) % gm;  // 256-row pair tile index
   const int tn = (tile % group_span) / gm;
   const int b = blockIdx.y;
@@ -580,20 +643,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (lane == 0) mbar_arrive_leader(smem_addr(&tempty[set]));
     }
     const int64_t row = (int64_t)tm * 256 + rank * 128 + q * 32 + lane;
-    if (row < g.M) {
-      float2* orow = out + ((int64_t)b * g.M + row) * g.N;
-      const int64_t col0 = (int64_t)tn * BN + h * 64;
-      if (col0 + 64 <= g.N && (g.N & 1) == 0) {
-        float4* dst = reinterpret_cast<float4*>(orow + col0);
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          dst[j] = make_float4(mre[2 * j], mim[2 * j], mre[2 * j + 1], mim[2 * j + 1]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 64; ++j)
-          if (col0 + j < g.N) orow[col0 + j] = make_float2(mre[j], mim[j]);
-      }
-    }
+    int64_t* gtab = reinterpret_cast<int64_t*>(smem);  // pipeline smem is free now
+    if (g.direct) build_gtab(g, gtab, (int64_t)tn * BN);
+    epilogue_store(g, out, (int64_t)b * g.M + row, row < g.M, (int64_t)tn * BN + h * 64, h * 64, mre,
+                   mim, gtab);
   }
   __syncwarp();
   tc_fence_before();
@@ -733,6 +786,16 @@ int gemm_choose_splits(int64_t batch, int64_t M, int64_t N, int64_t kp) {
 
 // k-blocks (of 16) accumulated in TMEM per promotion round; TNX_GEMM_PROMOTE
 // overrides (measured trade-off: accuracy vs TMEM-pipe load of the promotion).
+static int gemm_group_m() {
+  static int v = 0;
+  if (!v) {
+    const char* e = getenv("TNX_GEMM_GROUP_M");
+    v = e ? atoi(e) : GROUP_M;
+    if (v < 1) v = 1;
+  }
+  return v;
+}
+
 static int gemm_default_promote() {
   static int v = 0;
   if (!v) {
@@ -753,6 +816,12 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
   a.tiles_m = (int32_t)((g.M + BM - 1) / BM);
   a.tiles_n = (int32_t)((g.N + BN - 1) / BN);
   a.promote = g.promote > 0 ? g.promote : gemm_default_promote();
+  a.direct = g.direct;
+  a.dplanes = g.dplanes;
+  a.dplane_stride = g.dplane_stride;
+  a.fmap = g.fmap;
+  a.gmap = g.gmap;
+  a.group_m = gemm_group_m();
   const int splits = g.splits > 1 ? g.splits : 1;
   a.kb_per_split = (a.num_kb + splits - 1) / splits;
   a.partial = splits > 1 ? g.partial : nullptr;

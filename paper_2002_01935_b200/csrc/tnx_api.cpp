@@ -96,6 +96,7 @@ struct TensorLoc {
   int phase = 1;             // 0 hoist, 1 slice (work arena blocks)
   int block = -1;
   int64_t offset = 0;        // pool: element offset; persist: byte offset
+  bool fused = false;        // never materialised (written as parent operand planes)
 };
 
 enum VKind { VK_SIMT_T = 0, VK_SIMT_W = 1, VK_SIMT_S = 2, VK_GEMM = 3 };
@@ -112,6 +113,9 @@ struct Vertex {
   int blk_apl = -1, blk_bpl = -1, blk_part = -1;
   int splits = 1;
   bool swap = false;  // GEMM A operand taken from y (larger row count)
+  int direct_parent = -1;           // GEMM writes the parent's operand planes
+  int direct_side = -1;
+  bool side_direct[2] = {false, false};  // operand planes written by a child GEMM
   int64_t tab_off = -1;  // element offset in the sum-table buffer
 };
 
@@ -270,6 +274,23 @@ std::string u128_str(u128 v) {
   }
   std::reverse(s.begin(), s.end());
   return s;
+}
+
+// Label order of the K-blocked operand planes of GEMM vertex v, side 0 (A)
+// or 1 (B): row-major [K outer][batch + side rows][K inner, product 16].
+// False when K is padded or no K suffix has product 16 (gather-pack path).
+bool plane_order(const Plan& P, const Vertex& v, int side, std::vector<int>& dst) {
+  if (v.kp != v.K) return false;
+  int64_t pr = 1;
+  int i = (int)v.cl.size() - 1;
+  for (; i >= 0 && pr < 16; --i) pr *= P.dims[v.cl[i]];
+  if (pr != 16) return false;
+  const std::vector<int>& own = (side == 0) != v.swap ? v.ml : v.nl;
+  dst.assign(v.cl.begin(), v.cl.begin() + (i + 1));
+  dst.insert(dst.end(), v.bl.begin(), v.bl.end());
+  dst.insert(dst.end(), own.begin(), own.end());
+  dst.insert(dst.end(), v.cl.begin() + (i + 1), v.cl.end());
+  return true;
 }
 
 int compile(Plan& P, const tnx_plan_desc* D) {
@@ -530,6 +551,31 @@ int compile(Plan& P, const tnx_plan_desc* D) {
       if (v.splits > 1) v.blk_part = add_block(ph, 8 * (int64_t)v.splits * v.B * v.M * v.N, st, st);
     }
   }
+  // GEMM -> GEMM fusion: a child GEMM writes its result straight into the
+  // parent's split-TF32 operand planes (saves the parent's pack pass)
+  if (P.precision == TNX_PREC_3XTF32 && !(P.flags & TNX_FLAG_NO_DIRECT)) {
+    for (int k = 0; k < P.n - 1; ++k) {
+      Vertex& pv = P.V[k];
+      if (pv.kind != VK_GEMM) continue;
+      for (int side = 0; side < 2; ++side) {
+        const int c = side == 0 ? (pv.swap ? pv.b : pv.a) : (pv.swap ? pv.a : pv.b);
+        if (c < P.n) continue;
+        Vertex& cv = P.V[c - P.n];
+        if (cv.kind != VK_GEMM || cv.splits > 1 || cv.hoisted != pv.hoisted) continue;
+        std::vector<int> dst;
+        if (!plane_order(P, pv, side, dst)) continue;
+        cv.direct_parent = pv.ssa;
+        cv.direct_side = side;
+        pv.side_direct[side] = true;
+        const int ph = pv.hoisted ? 0 : 1;
+        Block& pb = P.blocks[ph][side == 0 ? pv.blk_apl : pv.blk_bpl];
+        pb.first = std::min(pb.first, step[c]);
+        TensorLoc& tc = P.T[c];
+        if (tc.arena == AR_WORK && tc.block >= 0) P.blocks[ph][tc.block].bytes = kAlign;
+        tc.fused = true;
+      }
+    }
+  }
   P.persist_bytes = std::max<int64_t>(persist_off, kAlign);
   P.work_bytes = std::max(pack_blocks(P.blocks[0]), pack_blocks(P.blocks[1]));
   P.work_bytes = std::max<int64_t>(P.work_bytes, kAlign);
@@ -698,21 +744,9 @@ int lower(Plan& P) {
           float* planes = side == 0 ? apl : bpl;
           const int64_t nrows = v.B * (side == 0 ? ra : rb);
           bool done = false;
-          // K-blocked plane layout = row-major order [K outer][rows][K inner = 16]
-          std::vector<int> k_in, k_out;
-          {
-            int64_t pr = 1;
-            int i = (int)v.cl.size() - 1;
-            for (; i >= 0 && pr < 16; --i) pr *= P.dims[v.cl[i]];
-            if (pr == 16) {
-              k_out.assign(v.cl.begin(), v.cl.begin() + (i + 1));
-              k_in.assign(v.cl.begin() + (i + 1), v.cl.end());
-            }
-          }
-          if (v.kp == v.K && !k_in.empty() && !(P.flags & TNX_FLAG_NO_TILED_PACK)) {
-            std::vector<int> dst = k_out;
-            dst.insert(dst.end(), rows.begin(), rows.end());
-            dst.insert(dst.end(), k_in.begin(), k_in.end());
+          if (v.side_direct[side]) continue;  // written by the child GEMM's epilogue
+          std::vector<int> dst;
+          if (plane_order(P, v, side, dst) && !(P.flags & TNX_FLAG_NO_TILED_PACK)) {
             PermParams pp;
             int64_t toff = 0;
             const size_t mark = P.ptabs.size();
@@ -748,6 +782,25 @@ int lower(Plan& P) {
         float2* part = v.splits > 1 ? reinterpret_cast<float2*>(P.block_ptr(phase, v.blk_part)) : nullptr;
         if (gemm_prepare(&g, apl, bpl, P.ptr(z), v.B, ra, rb, v.kp, v.splits, part, ebuf, sizeof(ebuf)))
           return fail(TNX_ERR_CUDA, std::string("vertex ") + std::to_string(v.ssa) + ": " + ebuf);
+        if (v.direct_parent >= 0) {
+          const Vertex& pv = P.V[v.direct_parent - P.n];
+          std::vector<int> pdst;
+          if (!plane_order(P, pv, v.direct_side, pdst))
+            return fail(TNX_ERR_INVALID, "direct planes: parent layout changed");
+          TensorLoc pl;
+          pl.labels = pdst;  // row-major strides of the parent's plane order
+          std::vector<int> crow = v.bl;
+          const std::vector<int>& first = v.swap ? v.nl : v.ml;
+          const std::vector<int>& second = v.swap ? v.ml : v.nl;
+          crow.insert(crow.end(), first.begin(), first.end());
+          if (!build_map(P, crow, &pl, nullptr, g.fmap, err) || !build_map(P, second, &pl, nullptr, g.gmap, err))
+            return fail(TNX_ERR_INVALID, "vertex " + std::to_string(v.ssa) + ": " + err);
+          const int64_t prows = pv.B * (v.direct_side == 0 ? (pv.swap ? pv.N : pv.M) : (pv.swap ? pv.M : pv.N));
+          g.direct = 1;
+          g.dplanes = reinterpret_cast<float*>(
+              P.block_ptr(phase, v.direct_side == 0 ? pv.blk_apl : pv.blk_bpl));
+          g.dplane_stride = prows * pv.kp;
+        }
         P.gemms.push_back(g);
         out.push_back({L_GEMM, (int)P.gemms.size() - 1, v.ssa});
       } else {
@@ -1039,7 +1092,7 @@ int tnx_stats_get(void* plan, tnx_stats* s) {
   for (int k : P.slice_order) {
     if (P.V[k].kind == VK_GEMM) {
       ++ng;
-      launches += P.V[k].splits > 1 ? 4 : 3;  // 2 packs + gemm (+ split-K reduce)
+      launches += (P.V[k].splits > 1 ? 4 : 3) - (int)P.V[k].side_direct[0] - (int)P.V[k].side_direct[1];
     } else {
       ++ns;
       launches += P.V[k].kind == VK_SIMT_S ? 2 : 1;
@@ -1078,6 +1131,9 @@ int tnx_debug_vertex(void* plan, uint64_t s, int32_t v, float* out_c64, int64_t 
   if (v < P.n || v >= nv) return fail(TNX_ERR_INVALID, "vertex must be internal");
   if ((u128)s >= P.d) return fail(TNX_ERR_INVALID, "slice out of range");
   const TensorLoc& t = P.T[v];
+  if (t.fused)
+    return fail(TNX_ERR_STATE, "vertex " + std::to_string(v) +
+                                   " is fused into its parent's operand planes (plan with TNX_FLAG_NO_DIRECT to dump it)");
   if (out_elems != t.size) return fail(TNX_ERR_INVALID, "size mismatch: need " + std::to_string(t.size));
   TNX_CUDA(cudaSetDevice(P.device));
   cudaStream_t st = P.own;

@@ -123,6 +123,14 @@ struct GemmPlan {
   int32_t splits;         // split-K factor (1 = none)
   int32_t two_sm;         // 2-CTA (cta_group::2) variant
   float2* partial;        // split-K workspace [splits][batch][M][N]
+  // direct planes: write the result as the parent GEMM's split-TF32 operand
+  // planes (offset = fmap(row) + gmap(col)) instead of complex64 `out`
+  int32_t direct;
+  int32_t pad;
+  float* dplanes;
+  int64_t dplane_stride;
+  IdxMap fmap;            // output row (batch*M + m) -> plane offset (st0)
+  IdxMap gmap;            // output column n -> plane offset (st0)
 };
 // Build tensor maps for planes laid out as [4][batch][M|N][kp] fp32; kp a
 // multiple of 16.

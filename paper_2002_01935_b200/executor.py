@@ -57,7 +57,7 @@ class SlicedPlan:
     """
 
     def __init__(self, tn, tree, slice_set=(), device=0, precision="3xtf32", graph=True,
-                 hoist=True, gemm_min_macs=0.0, tiled_pack=True):
+                 hoist=True, gemm_min_macs=0.0, tiled_pack=True, direct_planes=True):
         lib = nat.load()
         self.tn = tn
         self.tree = tree
@@ -90,7 +90,8 @@ class SlicedPlan:
             out=_i32([lid[l] for l in tn.output]), sl=_i32([lid[l] for l in self.sliced]))
         k = self._keep
         flags = ((0 if graph else nat.FLAG_NO_GRAPH) | (0 if hoist else nat.FLAG_NO_HOIST)
-                 | (0 if tiled_pack else nat.FLAG_NO_TILED_PACK))
+                 | (0 if tiled_pack else nat.FLAG_NO_TILED_PACK)
+                 | (0 if direct_planes else nat.FLAG_NO_DIRECT))
         if precision not in PRECISIONS:
             raise ValueError(f"unknown precision {precision!r}; choose from {sorted(PRECISIONS)}")
         self.precision = precision

@@ -97,7 +97,7 @@ def test_circuit_amplitude_sliced_gemm_path():
     m = metrics(tree, tn)
     ss = greedy_slice(tree, tn, min(m.width, 22) - 2, restarts=2)
     ref, _, _ = oracle.contract_sliced(tn, tree, ss.labels, slice_ids=range(0, 4))
-    plan = SlicedPlan(tn, tree, ss, gemm_min_macs=2 ** 16).bind()
+    plan = SlicedPlan(tn, tree, ss, gemm_min_macs=2 ** 16, direct_planes=False).bind()
     kinds = {v["kind"] for v in plan.vertex_info()}
     plan.run(0, 4)
     got = plan.result()
@@ -179,3 +179,22 @@ def test_tiled_pack_matches_gather_pack():
     ref, _, _ = oracle.contract_sliced(tn, tree, ss.labels, slice_ids=range(0, min(ss.d, 4)))
     for v in vals:
         assert rel_err(v, ref) <= TOL
+
+
+def test_direct_planes_fusion_matches_materialised():
+    """GEMM->GEMM operand-plane fusion gives the same slice values as the
+    fully materialised path (and dumps of fused vertices are refused)."""
+    from paper_2002_01935_b200.harness.workloads import load_workload
+    tn, tree, ss, _ = load_workload("cfg4p_7x7_d20", ws=21)
+    vals = []
+    for direct in (True, False):
+        plan = SlicedPlan(tn, tree, ss, gemm_min_macs=2 ** 14, direct_planes=direct).bind()
+        plan.run(0, 8)
+        vals.append(plan.result())
+        if direct:
+            fused = [v["ssa"] for v in plan.vertex_info() if v["kind"] == "gemm_tc"]
+            assert plan.stats()["num_gemm"] >= 2
+        plan.close()
+    assert rel_err(vals[0], vals[1]) <= 2e-6
+    ref, _, _ = oracle.contract_sliced(tn, tree, ss.labels, slice_ids=range(0, 8))
+    assert rel_err(vals[0], ref) <= TOL
