@@ -150,7 +150,7 @@ struct GemmArgs {
   float2* partial;       // split-K workspace [splits][batch][M][N] (nullptr: 1 split)
   int64_t rows_a, rows_b;  // batch * M, batch * N (rows per plane)
   int32_t direct;        // 1: store as the parent's split-TF32 planes
-  int32_t pad;
+  int32_t dvec;          // direct stores in float4 runs
   float* dplanes;
   int64_t dplane_stride;
   IdxMap fmap, gmap;
@@ -184,6 +184,28 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& g, float2* out, i
                                                const float (&mre)[64], const float (&mim)[64],
                                                const int64_t* gtab) {
   if (!row_ok) return;
+  if (g.direct && g.dvec && col0 + 64 <= g.N) {
+    const int64_t f = map_offset(g.fmap, grow);
+    float* d = g.dplanes;
+    const int64_t ps = g.dplane_stride;
+#pragma unroll
+    for (int j = 0; j < 64; j += 4) {
+      const int64_t off = f + gtab[hcol + j];
+      float rh[4], rl[4], ih[4], il[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        rh[t] = __uint_as_float(__float_as_uint(mre[j + t]) & 0xffffe000u);
+        ih[t] = __uint_as_float(__float_as_uint(mim[j + t]) & 0xffffe000u);
+        rl[t] = mre[j + t] - rh[t];
+        il[t] = mim[j + t] - ih[t];
+      }
+      *reinterpret_cast<float4*>(d + off) = make_float4(rh[0], rh[1], rh[2], rh[3]);
+      *reinterpret_cast<float4*>(d + off + ps) = make_float4(rl[0], rl[1], rl[2], rl[3]);
+      *reinterpret_cast<float4*>(d + off + 2 * ps) = make_float4(ih[0], ih[1], ih[2], ih[3]);
+      *reinterpret_cast<float4*>(d + off + 3 * ps) = make_float4(il[0], il[1], il[2], il[3]);
+    }
+    return;
+  }
   if (g.direct) {
     const int64_t f = map_offset(g.fmap, grow);
     float* d = g.dplanes;
@@ -817,6 +839,7 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
   a.tiles_n = (int32_t)((g.N + BN - 1) / BN);
   a.promote = g.promote > 0 ? g.promote : gemm_default_promote();
   a.direct = g.direct;
+  a.dvec = g.dvec;
   a.dplanes = g.dplanes;
   a.dplane_stride = g.dplane_stride;
   a.fmap = g.fmap;

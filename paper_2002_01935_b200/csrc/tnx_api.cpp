@@ -567,6 +567,24 @@ int compile(Plan& P, const tnx_plan_desc* D) {
         cv.direct_parent = pv.ssa;
         cv.direct_side = side;
         pv.side_direct[side] = true;
+        // the child's result is never materialised, so its row / column label
+        // orders are free: follow the parent's plane order (descending plane
+        // stride) so the epilogue stores contiguous runs
+        std::vector<int64_t> pst(P.L, 0);
+        int64_t acc = 1;
+        for (int i = (int)dst.size() - 1; i >= 0; --i) {
+          pst[dst[i]] = acc;
+          acc *= P.dims[dst[i]];
+        }
+        auto by_stride = [&](int a, int b) { return pst[a] > pst[b]; };
+        std::stable_sort(cv.ml.begin(), cv.ml.end(), by_stride);
+        std::stable_sort(cv.nl.begin(), cv.nl.end(), by_stride);
+        TensorLoc& zc = P.T[c];
+        zc.labels = cv.bl;
+        const std::vector<int>& f1 = cv.swap ? cv.nl : cv.ml;
+        const std::vector<int>& f2 = cv.swap ? cv.ml : cv.nl;
+        zc.labels.insert(zc.labels.end(), f1.begin(), f1.end());
+        zc.labels.insert(zc.labels.end(), f2.begin(), f2.end());
         const int ph = pv.hoisted ? 0 : 1;
         Block& pb = P.blocks[ph][side == 0 ? pv.blk_apl : pv.blk_bpl];
         pb.first = std::min(pb.first, step[c]);
@@ -800,6 +818,17 @@ int lower(Plan& P) {
           g.dplanes = reinterpret_cast<float*>(
               P.block_ptr(phase, v.direct_side == 0 ? pv.blk_apl : pv.blk_bpl));
           g.dplane_stride = prows * pv.kp;
+          // vector stores when every aligned group of 4 columns is contiguous
+          {
+            const IdxMap& gm = g.gmap;
+            bool vec = gm.n >= 1 && gm.st0[gm.n - 1] == 1 && gm.dim[gm.n - 1] % 4 == 0 && (v.N % 4) == 0 &&
+                       (g.dplane_stride % 4) == 0;
+            for (int i = 0; vec && i < gm.n - 1; ++i)
+              if (gm.st0[i] % 4) vec = false;
+            for (int i = 0; vec && i < g.fmap.n; ++i)
+              if (g.fmap.st0[i] % 4) vec = false;
+            g.dvec = vec ? 1 : 0;
+          }
         }
         P.gemms.push_back(g);
         out.push_back({L_GEMM, (int)P.gemms.size() - 1, v.ssa});

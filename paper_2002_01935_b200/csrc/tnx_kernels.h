@@ -126,7 +126,7 @@ struct GemmPlan {
   // direct planes: write the result as the parent GEMM's split-TF32 operand
   // planes (offset = fmap(row) + gmap(col)) instead of complex64 `out`
   int32_t direct;
-  int32_t pad;
+  int32_t dvec;           // direct stores as float4 runs of 4 columns
   float* dplanes;
   int64_t dplane_stride;
   IdxMap fmap;            // output row (batch*M + m) -> plane offset (st0)
