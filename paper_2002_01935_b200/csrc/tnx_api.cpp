@@ -552,24 +552,90 @@ int compile(Plan& P, const tnx_plan_desc* D) {
     }
   }
   // GEMM -> GEMM fusion: a child GEMM writes its result straight into the
-  // parent's split-TF32 operand planes (saves the parent's pack pass)
+  // parent's split-TF32 operand planes (saves the parent's pack pass).  The
+  // child's result is never materialised, so its orientation and row/column
+  // label orders are free; decided top-down (root first) so every parent's
+  // orientation is final before its children are arranged:
+  //   * the parent's K order puts 4 labels (product 16) that sit on ONE side
+  //     of the leading child innermost (they form the planes' 64 B K-inner run);
+  //   * that child side becomes the child's row (A) side, and the child's rows
+  //     and columns follow the parent's plane order, so the 32 lanes of an
+  //     epilogue warp store consecutive floats (whole 128 B lines).
   if (P.precision == TNX_PREC_3XTF32 && !(P.flags & TNX_FLAG_NO_DIRECT)) {
-    for (int k = 0; k < P.n - 1; ++k) {
+    auto in_list = [](const std::vector<int>& v, int l) {
+      return std::find(v.begin(), v.end(), l) != v.end();
+    };
+    auto refresh = [&](Vertex& v) {  // derived sizes after a swap / reorder
+      const int ph = v.hoisted ? 0 : 1;
+      const int64_t ra = v.swap ? v.N : v.M, rb = v.swap ? v.M : v.N;
+      P.blocks[ph][v.blk_apl].bytes = align_up(16 * v.B * ra * v.kp, kAlign);
+      P.blocks[ph][v.blk_bpl].bytes = align_up(16 * v.B * rb * v.kp, kAlign);
+      TensorLoc& z = P.T[v.ssa];
+      z.labels = v.bl;
+      const std::vector<int>& f1 = v.swap ? v.nl : v.ml;
+      const std::vector<int>& f2 = v.swap ? v.ml : v.nl;
+      z.labels.insert(z.labels.end(), f1.begin(), f1.end());
+      z.labels.insert(z.labels.end(), f2.begin(), f2.end());
+    };
+    for (int k = P.n - 2; k >= 0; --k) {
       Vertex& pv = P.V[k];
-      if (pv.kind != VK_GEMM) continue;
+      if (pv.kind != VK_GEMM || pv.kp != pv.K) continue;
+      int ch[2];
+      bool cand[2];
       for (int side = 0; side < 2; ++side) {
-        const int c = side == 0 ? (pv.swap ? pv.b : pv.a) : (pv.swap ? pv.a : pv.b);
-        if (c < P.n) continue;
-        Vertex& cv = P.V[c - P.n];
-        if (cv.kind != VK_GEMM || cv.splits > 1 || cv.hoisted != pv.hoisted) continue;
+        ch[side] = side == 0 ? (pv.swap ? pv.b : pv.a) : (pv.swap ? pv.a : pv.b);
+        cand[side] = false;
+        if (ch[side] < P.n) continue;
+        const Vertex& cv = P.V[ch[side] - P.n];
+        cand[side] = cv.kind == VK_GEMM && cv.splits == 1 && cv.hoisted == pv.hoisted;
+      }
+      if (!cand[0] && !cand[1]) continue;
+      // K-inner labels: product-16 run of parent K labels on one side of the lead child
+      const int lead = cand[0] ? 0 : 1;
+      Vertex& lc = P.V[ch[lead] - P.n];
+      std::vector<int> on_m, on_n;
+      for (int l : pv.cl) {
+        if (in_list(lc.ml, l)) on_m.push_back(l);
+        else if (in_list(lc.nl, l)) on_n.push_back(l);
+      }
+      std::vector<int> kin;
+      bool lead_rows_m = true;
+      for (int pass = 0; pass < 2 && kin.empty(); ++pass) {
+        const std::vector<int>& grp = (pass == 0) == (on_m.size() >= on_n.size()) ? on_m : on_n;
+        int64_t pr = 1;
+        std::vector<int> pick;
+        for (int i = (int)grp.size() - 1; i >= 0 && pr < 16; --i) {
+          pr *= P.dims[grp[i]];
+          pick.insert(pick.begin(), grp[i]);
+        }
+        if (pr == 16) {
+          kin = pick;
+          lead_rows_m = &grp == &on_m;
+        }
+      }
+      if (!kin.empty()) {
+        std::vector<int> ncl;
+        for (int l : pv.cl)
+          if (!in_list(kin, l)) ncl.push_back(l);
+        ncl.insert(ncl.end(), kin.begin(), kin.end());
+        pv.cl = ncl;
+      }
+      for (int side = 0; side < 2; ++side) {
+        if (!cand[side]) continue;
         std::vector<int> dst;
         if (!plane_order(P, pv, side, dst)) continue;
-        cv.direct_parent = pv.ssa;
-        cv.direct_side = side;
-        pv.side_direct[side] = true;
-        // the child's result is never materialised, so its row / column label
-        // orders are free: follow the parent's plane order (descending plane
-        // stride) so the epilogue stores contiguous runs
+        Vertex& cv = P.V[ch[side] - P.n];
+        // orientation: the child side holding the K-inner run becomes its rows
+        if (!kin.empty()) {
+          bool all_m = true, all_n = true;
+          for (int l : kin) {
+            all_m = all_m && in_list(cv.ml, l);
+            all_n = all_n && in_list(cv.nl, l);
+          }
+          if (side == lead) cv.swap = !lead_rows_m;
+          else if (all_m) cv.swap = false;
+          else if (all_n) cv.swap = true;
+        }
         std::vector<int64_t> pst(P.L, 0);
         int64_t acc = 1;
         for (int i = (int)dst.size() - 1; i >= 0; --i) {
@@ -579,16 +645,14 @@ int compile(Plan& P, const tnx_plan_desc* D) {
         auto by_stride = [&](int a, int b) { return pst[a] > pst[b]; };
         std::stable_sort(cv.ml.begin(), cv.ml.end(), by_stride);
         std::stable_sort(cv.nl.begin(), cv.nl.end(), by_stride);
-        TensorLoc& zc = P.T[c];
-        zc.labels = cv.bl;
-        const std::vector<int>& f1 = cv.swap ? cv.nl : cv.ml;
-        const std::vector<int>& f2 = cv.swap ? cv.ml : cv.nl;
-        zc.labels.insert(zc.labels.end(), f1.begin(), f1.end());
-        zc.labels.insert(zc.labels.end(), f2.begin(), f2.end());
+        refresh(cv);
+        cv.direct_parent = pv.ssa;
+        cv.direct_side = side;
+        pv.side_direct[side] = true;
         const int ph = pv.hoisted ? 0 : 1;
         Block& pb = P.blocks[ph][side == 0 ? pv.blk_apl : pv.blk_bpl];
-        pb.first = std::min(pb.first, step[c]);
-        TensorLoc& tc = P.T[c];
+        pb.first = std::min(pb.first, step[ch[side]]);
+        TensorLoc& tc = P.T[ch[side]];
         if (tc.arena == AR_WORK && tc.block >= 0) P.blocks[ph][tc.block].bytes = kAlign;
         tc.fused = true;
       }
