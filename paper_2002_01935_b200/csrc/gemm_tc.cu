@@ -146,7 +146,8 @@ struct GemmArgs {
   int32_t tiles_m, tiles_n;
   int32_t promote;       // k-blocks accumulated in TMEM before promotion
   int32_t group_m;       // rasterisation: M tiles per group
-  int32_t kb_per_split;  // split-K: k-blocks per CTA along grid.z
+  int32_t kb_per_split;  // split-K: k-blocks per work unit
+  int32_t splits;        // split-K slices (work units per tile)
   float2* partial;       // split-K workspace [splits][batch][M][N] (nullptr: 1 split)
   int64_t rows_a, rows_b;  // batch * M, batch * N (rows per plane)
   int32_t direct;        // 1: store as the parent's split-TF32 planes
@@ -255,206 +256,34 @@ __device__ __forceinline__ void mbar_arrive(uint32_t a) {
 // MMA issuer switches to the other TMEM accumulator set (double buffered,
 // 2 x 256 columns) while the epilogue warps add the finished set into FP32
 // registers with round-to-nearest ("promotion", as done for FP8 GEMMs).
+//
+// The kernel is persistent: each CTA (or CTA pair) walks work units
+// (tile, batch, split-K slice) with a stride of the grid; the smem ring and
+// the TMEM round counter run continuously across units, so the epilogue
+// stores of one tile overlap the first MMA rounds of the next.
+//
+// TWO_SM: a cluster of two CTAs on one TPC computes a 256 x 128 tile with
+// tcgen05.mma.cta_group::2 (M = 256) issued by the leader; each CTA stages
+// its own 128 A rows and half of the B tile (64 rows) per plane, so per-SM
+// shared-memory operand traffic per MMA drops from 8 KB to 6 KB.  TMA loads
+// of both CTAs complete on the leader's "full" barrier (peer bit cleared),
+// MMA commits multicast to both CTAs' "empty" / "tmem full" barriers, and
+// both CTAs' epilogue warps release a TMEM set on the leader's barrier.
 constexpr int NUM_THREADS = 320;
-
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    gemm_c64_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a,
-                           const __grid_constant__ CUtensorMap tm_b, const GemmArgs g) {
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  // [0,S) full  [S,2S) empty  [2S,2S+2) tmem_full  [2S+2,2S+4) tmem_empty
-  uint64_t* tfull = bars + 2 * STAGES;
-  uint64_t* tempty = bars + 2 * STAGES + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-
-  // grouped rasterisation of the (m, n) tile grid for L2 reuse
-  const int tile = blockIdx.x;
-  const int group_span = g.group_m * g.tiles_n;
-  const int group = tile / group_span;
-  const int first_m = group * g.group_m;
-  const int gm = min(g.tiles_m - first_m, g.group_m);
-  const int tm = first_m + (tile % group_span) % gm;
-  const int tn = (tile % group_span) / gm;
-  const int b = blockIdx.y;
-
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_addr(tmem_slot)),
-                 "r"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  if (threadIdx.x == 32) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(smem_addr(&bars[s]), 1);
-      mbar_init(smem_addr(&bars[STAGES + s]), 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(smem_addr(&tfull[s]), 1);
-      mbar_init(smem_addr(&tempty[s]), 8);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  const int kb_begin = blockIdx.z * g.kb_per_split;
-  const int nkb = min(g.num_kb - kb_begin, g.kb_per_split);  // k-blocks of this CTA
-  const int P = g.promote;
-  const int rounds = (nkb + P - 1) / P;
-  float2* const out = g.partial ? g.partial + (int64_t)blockIdx.z * g.batch * g.M * g.N : g.out;
-  if (warp == 0) {
-    if (lane == 0) {
-      // ---------------- TMA producer ----------------
-      const int row_a = (int)(b * g.M + (int64_t)tm * BM);
-      const int row_b = (int)(b * g.N + (int64_t)tn * BN);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(smem_addr(&bars[STAGES + stage]), phase ^ 1u);
-        const uint32_t full = smem_addr(&bars[stage]);
-        mbar_expect_tx(full, STAGE_BYTES);
-        unsigned char* sbase = smem + stage * STAGE_BYTES;
-        const int kbg = kb_begin + kb;  // global k-block
-#pragma unroll
-        for (int p = 0; p < 4; ++p) {
-          tma_load_3d(smem_addr(sbase + p * PLANE_BYTES), &tm_a, full, 0, row_a, p * g.num_kb + kbg);
-          tma_load_3d(smem_addr(sbase + (4 + p) * PLANE_BYTES), &tm_b, full, 0, row_b,
-                      p * g.num_kb + kbg);
-        }
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1u;
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
-      constexpr uint32_t ID_POS = idesc_tf32(false);
-      constexpr uint32_t ID_NEG = idesc_tf32(true);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int r = 0; r < rounds; ++r) {
-        const int set = r & 1;
-        mbar_wait(smem_addr(&tempty[set]), ((uint32_t)(r >> 1) & 1u) ^ 1u);
-        tc_fence_after();
-        const uint32_t d_re = tmem_base + set * 256;
-        const uint32_t d_im = d_re + BN;
-        const int kb0 = r * P;
-        const int kb1 = min(nkb, kb0 + P);
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(smem_addr(&bars[stage]), phase);
-          tc_fence_after();
-          const uint32_t sb = smem_addr(smem + stage * STAGE_BYTES);
-#pragma unroll
-          for (int ks = 0; ks < BK / 8; ++ks) {
-            const uint32_t koff = ks * 32;  // bytes within the 64 B swizzled row
-            const uint64_t ar_h = umma_desc_sw64(sb + 0 * PLANE_BYTES + koff);
-            const uint64_t ar_l = umma_desc_sw64(sb + 1 * PLANE_BYTES + koff);
-            const uint64_t ai_h = umma_desc_sw64(sb + 2 * PLANE_BYTES + koff);
-            const uint64_t ai_l = umma_desc_sw64(sb + 3 * PLANE_BYTES + koff);
-            const uint64_t br_h = umma_desc_sw64(sb + 4 * PLANE_BYTES + koff);
-            const uint64_t br_l = umma_desc_sw64(sb + 5 * PLANE_BYTES + koff);
-            const uint64_t bi_h = umma_desc_sw64(sb + 6 * PLANE_BYTES + koff);
-            const uint64_t bi_l = umma_desc_sw64(sb + 7 * PLANE_BYTES + koff);
-            const uint32_t acc0 = (kb > kb0 || ks > 0) ? 1u : 0u;
-            // small cross terms first
-            umma_tf32(d_re, ar_h, br_l, ID_POS, acc0);
-            umma_tf32(d_re, ar_l, br_h, ID_POS, 1u);
-            umma_tf32(d_re, ai_h, bi_l, ID_NEG, 1u);
-            umma_tf32(d_re, ai_l, bi_h, ID_NEG, 1u);
-            umma_tf32(d_re, ar_h, br_h, ID_POS, 1u);
-            umma_tf32(d_re, ai_h, bi_h, ID_NEG, 1u);
-            umma_tf32(d_im, ar_h, bi_l, ID_POS, acc0);
-            umma_tf32(d_im, ar_l, bi_h, ID_POS, 1u);
-            umma_tf32(d_im, ai_h, br_l, ID_POS, 1u);
-            umma_tf32(d_im, ai_l, br_h, ID_POS, 1u);
-            umma_tf32(d_im, ar_h, bi_h, ID_POS, 1u);
-            umma_tf32(d_im, ai_h, br_h, ID_POS, 1u);
-          }
-          umma_commit(smem_addr(&bars[STAGES + stage]));  // frees the smem stage
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1u;
-          }
-        }
-        umma_commit(smem_addr(&tfull[set]));  // this accumulator set is complete
-      }
-    }
-  } else {
-    // ---------------- promotion + epilogue (8 warps) ----------------
-    const int q = warp & 3;          // TMEM lane quarter this warp may access
-    const int h = (warp - 2) >> 2;   // column half
-    float mre[64], mim[64];
-#pragma unroll
-    for (int j = 0; j < 64; ++j) {
-      mre[j] = 0.f;
-      mim[j] = 0.f;
-    }
-    const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16) + h * 64;
-    for (int r = 0; r < rounds; ++r) {
-      const int set = r & 1;
-      mbar_wait(smem_addr(&tfull[set]), (uint32_t)(r >> 1) & 1u);
-      tc_fence_after();
-      const uint32_t t0 = lane_base + set * 256;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        uint32_t re[16], im[16];
-        tmem_ld16(t0 + j * 16, re);
-        tmem_ld16(t0 + BN + j * 16, im);
-        tmem_wait_ld();
-#pragma unroll
-        for (int t = 0; t < 16; ++t) {
-          mre[j * 16 + t] += __uint_as_float(re[t]);
-          mim[j * 16 + t] += __uint_as_float(im[t]);
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_addr(&tempty[set]));
-    }
-    const int64_t row = (int64_t)tm * BM + q * 32 + lane;
-    int64_t* gtab = reinterpret_cast<int64_t*>(smem);  // pipeline smem is free now
-    if (g.direct) build_gtab(g, gtab, (int64_t)tn * BN);
-    epilogue_store(g, out, (int64_t)b * g.M + row, row < g.M, (int64_t)tn * BN + h * 64, h * 64, mre,
-                   mim, gtab);
-  }
-  __syncwarp();
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(TMEM_COLS)
-                 : "memory");
-  }
-}
-
-// ---------------------------------------------------------------------------
-// 2-CTA variant (cta_group::2): a cluster of two CTAs on one TPC computes a
-// 256 x 128 complex tile.  Each CTA stages its own 128 A rows and half of the
-// B tile (64 rows) per plane; the leader CTA issues M=256 MMAs that read A
-// from both CTAs and exchange the B halves, so per-SM shared-memory operand
-// traffic per MMA drops from 8 KB to 6 KB.  TMA loads of both CTAs complete
-// on the leader's "full" barrier (peer bit cleared), MMA commits multicast to
-// both CTAs' "empty" / "tmem full" barriers, and both CTAs' epilogue warps
-// release a TMEM accumulator set by arriving on the leader's barrier.
 constexpr int BN_HALF = BN / 2;
-constexpr int A2_BYTES = BM * BK * 4;         // 8 KB per A plane (128 rows)
-constexpr int B2_BYTES = BN_HALF * BK * 4;    // 4 KB per B plane (64 rows)
-constexpr int STAGE2_BYTES = 4 * A2_BYTES + 4 * B2_BYTES;   // 48 KB
-constexpr int STAGES2 = 4;
-constexpr int SMEM2_BYTES = STAGES2 * STAGE2_BYTES + 1024 + 256;
 constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;
+
+template <bool TWO_SM>
+struct KCfg {
+  static constexpr int A_BYTES = BM * BK * 4;                          // 8 KB
+  static constexpr int B_BYTES = (TWO_SM ? BN_HALF : BN) * BK * 4;     // 4 / 8 KB
+  static constexpr int STAGE = 4 * A_BYTES + 4 * B_BYTES;              // 48 / 64 KB
+  static constexpr int NSTAGE = TWO_SM ? 4 : 3;
+  static constexpr int GTAB_OFF = NSTAGE * STAGE;                      // 1 KB column table
+  static constexpr int BAR_OFF = GTAB_OFF + BN * 8;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static constexpr int TILE_M = TWO_SM ? 256 : BM;
+};
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -492,192 +321,263 @@ __device__ __forceinline__ void mbar_arrive_leader(uint32_t local_addr) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(0));
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
-// M=256 (pair), N=128, D=f32, A=B=tf32 K-major.
-__host__ __device__ constexpr uint32_t idesc_tf32_2sm(bool neg_a) {
+// idesc: D=f32, A=B=tf32, K-major, N=128, M=128 (1 CTA) or 256 (pair)
+template <bool TWO_SM>
+__host__ __device__ constexpr uint32_t idesc_mma(bool neg_a) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((neg_a ? 1u : 0u) << 13) |
-         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((TWO_SM ? 256 : BM) >> 4) << 24);
 }
 
+// work unit -> (split z, batch b, tile row tm, tile column tn)
+__device__ __forceinline__ void decode_unit(const GemmArgs& g, int u, int& z, int& b, int& tm, int& tn) {
+  const int tiles = g.tiles_m * g.tiles_n;
+  const int t = u % tiles;
+  const int zb = u / tiles;
+  b = zb % (int)g.batch;
+  z = zb / (int)g.batch;
+  const int group_span = g.group_m * g.tiles_n;
+  const int group = t / group_span;
+  const int first_m = group * g.group_m;
+  const int gm = min(g.tiles_m - first_m, g.group_m);
+  tm = first_m + (t % group_span) % gm;
+  tn = (t % group_span) / gm;
+}
+
+template <bool TWO_SM>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-    gemm_c64_3xtf32_2sm_kernel(const __grid_constant__ CUtensorMap tm_a,
-                               const __grid_constant__ CUtensorMap tm_b, const GemmArgs g) {
+    gemm_c64_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a,
+                           const __grid_constant__ CUtensorMap tm_b, const GemmArgs g) {
+  using C = KCfg<TWO_SM>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES);
-  uint64_t* tfull = bars + 2 * STAGES2;
-  uint64_t* tempty = bars + 2 * STAGES2 + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES2 + 4);
+  int64_t* gtab = reinterpret_cast<int64_t*>(smem + C::GTAB_OFF);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + C::NSTAGE;
+  uint64_t* tfull = bars + 2 * C::NSTAGE;
+  uint64_t* tempty = bars + 2 * C::NSTAGE + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::NSTAGE + 4);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();
+  const uint32_t rank = TWO_SM ? cluster_rank() : 0u;
   const bool leader = rank == 0;
-
-  // pair tile (grouped rasterisation over 256-row pair tiles)
-  const int tile = blockIdx.x >> 1;
-  const int group_span = g.group_m * g.tiles_n;
-  const int group = tile / group_span;
-  const int first_m = group * g.group_m;
-  const int gm = min(g.tiles_m - first_m, g.group_m);
-  const int tm = first_m + (tile % group_span) % gm;  // 256-row pair tile index
-  const int tn = (tile % group_span) / gm;
-  const int b = blockIdx.y;
+  const int cid = TWO_SM ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int ncta = TWO_SM ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int units = g.tiles_m * g.tiles_n * (int)g.batch * g.splits;
 
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_addr(tmem_slot)),
-                 "r"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    if constexpr (TWO_SM) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_addr(tmem_slot)), "r"(TMEM_COLS) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_addr(tmem_slot)), "r"(TMEM_COLS) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   if (threadIdx.x == 32) {
-    for (int s = 0; s < STAGES2; ++s) {
-      mbar_init(smem_addr(&bars[s]), 1);
-      mbar_init(smem_addr(&bars[STAGES2 + s]), 1);
+    for (int s = 0; s < C::NSTAGE; ++s) {
+      mbar_init(smem_addr(&full[s]), 1);
+      mbar_init(smem_addr(&empty[s]), 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(smem_addr(&tfull[s]), 1);
-      mbar_init(smem_addr(&tempty[s]), 16);
+      mbar_init(smem_addr(&tempty[s]), TWO_SM ? 16 : 8);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   tc_fence_before();
-  cluster_sync_all();
+  if constexpr (TWO_SM) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-
-  const int kb_begin = blockIdx.z * g.kb_per_split;
-  const int nkb = min(g.num_kb - kb_begin, g.kb_per_split);
   const int P = g.promote;
-  const int rounds = (nkb + P - 1) / P;
-  float2* const out = g.partial ? g.partial + (int64_t)blockIdx.z * g.batch * g.M * g.N : g.out;
+
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer (both CTAs) ----------------
-      const int row_a = (int)(b * g.M + (int64_t)tm * 256 + rank * 128);
-      const int row_b = (int)(b * g.N + (int64_t)tn * BN + rank * BN_HALF);
+      // ---------------- TMA producer ----------------
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(smem_addr(&bars[STAGES2 + stage]), phase ^ 1u);
-        const uint32_t full = smem_addr(&bars[stage]);
-        if (leader) mbar_expect_tx(full, 2 * STAGE2_BYTES);
-        unsigned char* sbase = smem + stage * STAGE2_BYTES;
-        const int kbg = kb_begin + kb;  // global k-block
+      for (int u = cid; u < units; u += ncta) {
+        int z, b, tm, tn;
+        decode_unit(g, u, z, b, tm, tn);
+        const int kb_begin = z * g.kb_per_split;
+        const int nkb = min(g.num_kb - kb_begin, g.kb_per_split);
+        const int row_a = (int)(b * g.M + (int64_t)tm * C::TILE_M + rank * BM);
+        const int row_b = (int)(b * g.N + (int64_t)tn * BN + rank * BN_HALF);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(smem_addr(&empty[stage]), phase ^ 1u);
+          const uint32_t fb = smem_addr(&full[stage]);
+          if (leader) mbar_expect_tx(fb, (TWO_SM ? 2 : 1) * C::STAGE);
+          unsigned char* sbase = smem + stage * C::STAGE;
+          const int kbg = kb_begin + kb;
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
-          tma_load_3d_2sm(smem_addr(sbase + p * A2_BYTES), &tm_a, full, 0, row_a, p * g.num_kb + kbg);
-          tma_load_3d_2sm(smem_addr(sbase + 4 * A2_BYTES + p * B2_BYTES), &tm_b, full, 0, row_b,
+          for (int p = 0; p < 4; ++p) {
+            if constexpr (TWO_SM) {
+              tma_load_3d_2sm(smem_addr(sbase + p * C::A_BYTES), &tm_a, fb, 0, row_a, p * g.num_kb + kbg);
+              tma_load_3d_2sm(smem_addr(sbase + 4 * C::A_BYTES + p * C::B_BYTES), &tm_b, fb, 0, row_b,
+                              p * g.num_kb + kbg);
+            } else {
+              tma_load_3d(smem_addr(sbase + p * C::A_BYTES), &tm_a, fb, 0, row_a, p * g.num_kb + kbg);
+              tma_load_3d(smem_addr(sbase + 4 * C::A_BYTES + p * C::B_BYTES), &tm_b, fb, 0, row_b,
                           p * g.num_kb + kbg);
-        }
-        if (++stage == STAGES2) {
-          stage = 0;
-          phase ^= 1u;
+            }
+          }
+          if (++stage == C::NSTAGE) {
+            stage = 0;
+            phase ^= 1u;
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {
-      // ---------------- MMA issuer (leader CTA) ----------------
-      constexpr uint32_t ID_POS = idesc_tf32_2sm(false);
-      constexpr uint32_t ID_NEG = idesc_tf32_2sm(true);
+      // ---------------- MMA issuer ----------------
+      constexpr uint32_t ID_POS = idesc_mma<TWO_SM>(false);
+      constexpr uint32_t ID_NEG = idesc_mma<TWO_SM>(true);
       int stage = 0;
       uint32_t phase = 0;
-      for (int r = 0; r < rounds; ++r) {
-        const int set = r & 1;
-        mbar_wait(smem_addr(&tempty[set]), ((uint32_t)(r >> 1) & 1u) ^ 1u);
-        tc_fence_after();
-        const uint32_t d_re = tmem_base + set * 256;
-        const uint32_t d_im = d_re + BN;
-        const int kb0 = r * P;
-        const int kb1 = min(nkb, kb0 + P);
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(smem_addr(&bars[stage]), phase);
+      uint32_t R = 0;  // global accumulator-round counter
+      for (int u = cid; u < units; u += ncta) {
+        int z, b, tm, tn;
+        decode_unit(g, u, z, b, tm, tn);
+        const int kb_begin = z * g.kb_per_split;
+        const int nkb = min(g.num_kb - kb_begin, g.kb_per_split);
+        const int rounds = (nkb + P - 1) / P;
+        for (int r = 0; r < rounds; ++r, ++R) {
+          const uint32_t set = R & 1u;
+          mbar_wait(smem_addr(&tempty[set]), ((R >> 1) & 1u) ^ 1u);
           tc_fence_after();
-          const uint32_t sb = smem_addr(smem + stage * STAGE2_BYTES);
+          const uint32_t d_re = tmem_base + set * 256;
+          const uint32_t d_im = d_re + BN;
+          const int kb0 = r * P;
+          const int kb1 = min(nkb, kb0 + P);
+          for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(smem_addr(&full[stage]), phase);
+            tc_fence_after();
+            const uint32_t sb = smem_addr(smem + stage * C::STAGE);
 #pragma unroll
-          for (int ks = 0; ks < BK / 8; ++ks) {
-            const uint32_t koff = ks * 32;
-            const uint64_t ar_h = umma_desc_sw64(sb + 0 * A2_BYTES + koff);
-            const uint64_t ar_l = umma_desc_sw64(sb + 1 * A2_BYTES + koff);
-            const uint64_t ai_h = umma_desc_sw64(sb + 2 * A2_BYTES + koff);
-            const uint64_t ai_l = umma_desc_sw64(sb + 3 * A2_BYTES + koff);
-            const uint32_t bb = sb + 4 * A2_BYTES + koff;
-            const uint64_t br_h = umma_desc_sw64(bb + 0 * B2_BYTES);
-            const uint64_t br_l = umma_desc_sw64(bb + 1 * B2_BYTES);
-            const uint64_t bi_h = umma_desc_sw64(bb + 2 * B2_BYTES);
-            const uint64_t bi_l = umma_desc_sw64(bb + 3 * B2_BYTES);
-            const uint32_t acc0 = (kb > kb0 || ks > 0) ? 1u : 0u;
-            umma_tf32_2sm(d_re, ar_h, br_l, ID_POS, acc0);
-            umma_tf32_2sm(d_re, ar_l, br_h, ID_POS, 1u);
-            umma_tf32_2sm(d_re, ai_h, bi_l, ID_NEG, 1u);
-            umma_tf32_2sm(d_re, ai_l, bi_h, ID_NEG, 1u);
-            umma_tf32_2sm(d_re, ar_h, br_h, ID_POS, 1u);
-            umma_tf32_2sm(d_re, ai_h, bi_h, ID_NEG, 1u);
-            umma_tf32_2sm(d_im, ar_h, bi_l, ID_POS, acc0);
-            umma_tf32_2sm(d_im, ar_l, bi_h, ID_POS, 1u);
-            umma_tf32_2sm(d_im, ai_h, br_l, ID_POS, 1u);
-            umma_tf32_2sm(d_im, ai_l, br_h, ID_POS, 1u);
-            umma_tf32_2sm(d_im, ar_h, bi_h, ID_POS, 1u);
-            umma_tf32_2sm(d_im, ai_h, br_h, ID_POS, 1u);
+            for (int ks = 0; ks < BK / 8; ++ks) {
+              const uint32_t koff = ks * 32;
+              const uint64_t ar_h = umma_desc_sw64(sb + 0 * C::A_BYTES + koff);
+              const uint64_t ar_l = umma_desc_sw64(sb + 1 * C::A_BYTES + koff);
+              const uint64_t ai_h = umma_desc_sw64(sb + 2 * C::A_BYTES + koff);
+              const uint64_t ai_l = umma_desc_sw64(sb + 3 * C::A_BYTES + koff);
+              const uint32_t bb = sb + 4 * C::A_BYTES + koff;
+              const uint64_t br_h = umma_desc_sw64(bb + 0 * C::B_BYTES);
+              const uint64_t br_l = umma_desc_sw64(bb + 1 * C::B_BYTES);
+              const uint64_t bi_h = umma_desc_sw64(bb + 2 * C::B_BYTES);
+              const uint64_t bi_l = umma_desc_sw64(bb + 3 * C::B_BYTES);
+              const uint32_t acc0 = (kb > kb0 || ks > 0) ? 1u : 0u;
+              if constexpr (TWO_SM) {
+                umma_tf32_2sm(d_re, ar_h, br_l, ID_POS, acc0);
+                umma_tf32_2sm(d_re, ar_l, br_h, ID_POS, 1u);
+                umma_tf32_2sm(d_re, ai_h, bi_l, ID_NEG, 1u);
+                umma_tf32_2sm(d_re, ai_l, bi_h, ID_NEG, 1u);
+                umma_tf32_2sm(d_re, ar_h, br_h, ID_POS, 1u);
+                umma_tf32_2sm(d_re, ai_h, bi_h, ID_NEG, 1u);
+                umma_tf32_2sm(d_im, ar_h, bi_l, ID_POS, acc0);
+                umma_tf32_2sm(d_im, ar_l, bi_h, ID_POS, 1u);
+                umma_tf32_2sm(d_im, ai_h, br_l, ID_POS, 1u);
+                umma_tf32_2sm(d_im, ai_l, br_h, ID_POS, 1u);
+                umma_tf32_2sm(d_im, ar_h, bi_h, ID_POS, 1u);
+                umma_tf32_2sm(d_im, ai_h, br_h, ID_POS, 1u);
+              } else {
+                umma_tf32(d_re, ar_h, br_l, ID_POS, acc0);
+                umma_tf32(d_re, ar_l, br_h, ID_POS, 1u);
+                umma_tf32(d_re, ai_h, bi_l, ID_NEG, 1u);
+                umma_tf32(d_re, ai_l, bi_h, ID_NEG, 1u);
+                umma_tf32(d_re, ar_h, br_h, ID_POS, 1u);
+                umma_tf32(d_re, ai_h, bi_h, ID_NEG, 1u);
+                umma_tf32(d_im, ar_h, bi_l, ID_POS, acc0);
+                umma_tf32(d_im, ar_l, bi_h, ID_POS, 1u);
+                umma_tf32(d_im, ai_h, br_l, ID_POS, 1u);
+                umma_tf32(d_im, ai_l, br_h, ID_POS, 1u);
+                umma_tf32(d_im, ar_h, bi_h, ID_POS, 1u);
+                umma_tf32(d_im, ai_h, br_h, ID_POS, 1u);
+              }
+            }
+            if constexpr (TWO_SM) umma_commit_2sm(smem_addr(&empty[stage]));
+            else umma_commit(smem_addr(&empty[stage]));
+            if (++stage == C::NSTAGE) {
+              stage = 0;
+              phase ^= 1u;
+            }
           }
-          umma_commit_2sm(smem_addr(&bars[STAGES2 + stage]));
-          if (++stage == STAGES2) {
-            stage = 0;
-            phase ^= 1u;
-          }
+          if constexpr (TWO_SM) umma_commit_2sm(smem_addr(&tfull[set]));
+          else umma_commit(smem_addr(&tfull[set]));
         }
-        umma_commit_2sm(smem_addr(&tfull[set]));
       }
     }
   } else {
     // ---------------- promotion + epilogue (8 warps per CTA) ----------------
-    const int q = warp & 3;
-    const int h = (warp - 2) >> 2;
-    float mre[64], mim[64];
-#pragma unroll
-    for (int j = 0; j < 64; ++j) {
-      mre[j] = 0.f;
-      mim[j] = 0.f;
-    }
+    const int q = warp & 3;          // TMEM lane quarter this warp may access
+    const int h = (warp - 2) >> 2;   // column half
     const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16) + h * 64;
-    for (int r = 0; r < rounds; ++r) {
-      const int set = r & 1;
-      mbar_wait(smem_addr(&tfull[set]), (uint32_t)(r >> 1) & 1u);
-      tc_fence_after();
-      const uint32_t t0 = lane_base + set * 256;
+    uint32_t R = 0;
+    for (int u = cid; u < units; u += ncta) {
+      int z, b, tm, tn;
+      decode_unit(g, u, z, b, tm, tn);
+      const int kb_begin = z * g.kb_per_split;
+      const int nkb = min(g.num_kb - kb_begin, g.kb_per_split);
+      const int rounds = (nkb + P - 1) / P;
+      float mre[64], mim[64];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        uint32_t re[16], im[16];
-        tmem_ld16(t0 + j * 16, re);
-        tmem_ld16(t0 + BN + j * 16, im);
-        tmem_wait_ld();
+      for (int j = 0; j < 64; ++j) {
+        mre[j] = 0.f;
+        mim[j] = 0.f;
+      }
+      for (int r = 0; r < rounds; ++r, ++R) {
+        const uint32_t set = R & 1u;
+        mbar_wait(smem_addr(&tfull[set]), (R >> 1) & 1u);
+        tc_fence_after();
+        const uint32_t t0 = lane_base + set * 256;
 #pragma unroll
-        for (int t = 0; t < 16; ++t) {
-          mre[j * 16 + t] += __uint_as_float(re[t]);
-          mim[j * 16 + t] += __uint_as_float(im[t]);
+        for (int j = 0; j < 4; ++j) {
+          uint32_t re[16], im[16];
+          tmem_ld16(t0 + j * 16, re);
+          tmem_ld16(t0 + BN + j * 16, im);
+          tmem_wait_ld();
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            mre[j * 16 + t] += __uint_as_float(re[t]);
+            mim[j * 16 + t] += __uint_as_float(im[t]);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (TWO_SM) mbar_arrive_leader(smem_addr(&tempty[set]));
+          else mbar_arrive(smem_addr(&tempty[set]));
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_leader(smem_addr(&tempty[set]));
+      float2* const out = g.partial ? g.partial + (int64_t)z * g.batch * g.M * g.N : g.out;
+      const int64_t row = (int64_t)tm * C::TILE_M + rank * BM + q * 32 + lane;
+      if (g.direct) {
+        asm volatile("bar.sync 1, 256;" ::: "memory");  // previous unit's stores done with gtab
+        const int e = threadIdx.x - 64;
+        const int64_t cb = (int64_t)tn * BN;
+        if (e < BN) gtab[e] = (cb + e < g.N) ? map_offset(g.gmap, cb + e) : 0;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+      }
+      epilogue_store(g, out, (int64_t)b * g.M + row, row < g.M, (int64_t)tn * BN + h * 64, h * 64, mre,
+                     mim, gtab);
     }
-    const int64_t row = (int64_t)tm * 256 + rank * 128 + q * 32 + lane;
-    int64_t* gtab = reinterpret_cast<int64_t*>(smem);  // pipeline smem is free now
-    if (g.direct) build_gtab(g, gtab, (int64_t)tn * BN);
-    epilogue_store(g, out, (int64_t)b * g.M + row, row < g.M, (int64_t)tn * BN + h * 64, h * 64, mre,
-                   mim, gtab);
   }
   __syncwarp();
   tc_fence_before();
-  cluster_sync_all();
+  if constexpr (TWO_SM) cluster_sync_all(); else __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(TMEM_COLS)
-                 : "memory");
+    if constexpr (TWO_SM)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                   : "memory");
   }
 }
 
@@ -738,11 +638,11 @@ int gemm_use_2sm(int64_t batch, int64_t M, int64_t N, int64_t kp) {
 }
 
 int gemm_init_attributes(char* err, size_t errlen) {
-  cudaError_t e = cudaFuncSetAttribute(gemm_c64_3xtf32_2sm_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
+  cudaError_t e = cudaFuncSetAttribute(gemm_c64_3xtf32_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, KCfg<true>::SMEM);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(gemm_c64_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             SMEM_BYTES);
+    e = cudaFuncSetAttribute(gemm_c64_3xtf32_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             KCfg<false>::SMEM);
   if (e != cudaSuccess) {
     snprintf(err, errlen, "cudaFuncSetAttribute(gemm): %s", cudaGetErrorString(e));
     return 1;
@@ -851,27 +751,32 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
   a.rows_a = g.batch * g.M;
   a.rows_b = g.batch * g.N;
   const int zs = (a.num_kb + a.kb_per_split - 1) / a.kb_per_split;
+  a.splits = zs;
   const CUtensorMap* ta = reinterpret_cast<const CUtensorMap*>(g.tmap_a);
   const CUtensorMap* tb = reinterpret_cast<const CUtensorMap*>(g.tmap_b);
+  if (g.two_sm) a.tiles_m = (int32_t)((g.M + 255) / 256);
+  const int64_t units = (int64_t)a.tiles_m * a.tiles_n * g.batch * zs;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
   if (g.two_sm) {
-    a.tiles_m = (int32_t)((g.M + 255) / 256);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(2 * a.tiles_m * a.tiles_n), (unsigned)g.batch, (unsigned)zs);
-    cfg.blockDim = dim3(NUM_THREADS);
-    cfg.dynamicSmemBytes = SMEM2_BYTES;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    const int64_t clusters = std::min<int64_t>(units, 74);
+    cfg.gridDim = dim3((unsigned)(2 * clusters));
+    cfg.dynamicSmemBytes = KCfg<true>::SMEM;
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t le = cudaLaunchKernelEx(&cfg, gemm_c64_3xtf32_2sm_kernel, *ta, *tb, a);
+    cudaError_t le = cudaLaunchKernelEx(&cfg, gemm_c64_3xtf32_kernel<true>, *ta, *tb, a);
     if (le != cudaSuccess) return le;
   } else {
-    dim3 grid((unsigned)(a.tiles_m * a.tiles_n), (unsigned)g.batch, (unsigned)zs);
-    gemm_c64_3xtf32_kernel<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(*ta, *tb, a);
+    cfg.gridDim = dim3((unsigned)std::min<int64_t>(units, 148));
+    cfg.dynamicSmemBytes = KCfg<false>::SMEM;
+    cudaError_t le = cudaLaunchKernelEx(&cfg, gemm_c64_3xtf32_kernel<false>, *ta, *tb, a);
+    if (le != cudaSuccess) return le;
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || zs == 1) return e;
