@@ -20,6 +20,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <memory>
 #include <string>
 #include <vector>
@@ -590,27 +591,52 @@ int compile(Plan& P, const tnx_plan_desc* D) {
         cand[side] = cv.kind == VK_GEMM && cv.splits == 1 && cv.hoisted == pv.hoisted;
       }
       if (!cand[0] && !cand[1]) continue;
-      // K-inner labels: product-16 run of parent K labels on one side of the lead child
+      // K-inner labels: a product-16 run of parent K labels lying on ONE side
+      // of each fused child (prefer a run that works for both children)
       const int lead = cand[0] ? 0 : 1;
-      Vertex& lc = P.V[ch[lead] - P.n];
-      std::vector<int> on_m, on_n;
-      for (int l : pv.cl) {
-        if (in_list(lc.ml, l)) on_m.push_back(l);
-        else if (in_list(lc.nl, l)) on_n.push_back(l);
-      }
       std::vector<int> kin;
-      bool lead_rows_m = true;
-      for (int pass = 0; pass < 2 && kin.empty(); ++pass) {
-        const std::vector<int>& grp = (pass == 0) == (on_m.size() >= on_n.size()) ? on_m : on_n;
+      int side_of[2] = {-1, -1};  // per child: 0 = its ml side, 1 = its nl side
+      auto pick16 = [&](const std::vector<int>& grp) {
         int64_t pr = 1;
         std::vector<int> pick;
         for (int i = (int)grp.size() - 1; i >= 0 && pr < 16; --i) {
           pr *= P.dims[grp[i]];
           pick.insert(pick.begin(), grp[i]);
         }
-        if (pr == 16) {
-          kin = pick;
-          lead_rows_m = &grp == &on_m;
+        return pr == 16 ? pick : std::vector<int>();
+      };
+      {
+        int best = -1;
+        for (int s0 = 0; s0 < 2; ++s0)
+          for (int s1 = 0; s1 < (cand[0] && cand[1] ? 2 : 1); ++s1) {
+            std::vector<int> grp;
+            for (int l : pv.cl) {
+              bool ok = true;
+              for (int side = 0; side < 2; ++side) {
+                if (!cand[side]) continue;
+                const Vertex& cv = P.V[ch[side] - P.n];
+                const int want = (side == lead) ? s0 : s1;
+                ok = ok && in_list(want == 0 ? cv.ml : cv.nl, l);
+              }
+              if (ok) grp.push_back(l);
+            }
+            std::vector<int> pk = pick16(grp);
+            if (!pk.empty() && (int)grp.size() > best) {
+              best = (int)grp.size();
+              kin = pk;
+              side_of[lead] = s0;
+              side_of[1 - lead] = s1;
+            }
+          }
+        if (kin.empty()) {  // lead child only
+          const Vertex& lc = P.V[ch[lead] - P.n];
+          for (int s0 = 0; s0 < 2 && kin.empty(); ++s0) {
+            std::vector<int> grp;
+            for (int l : pv.cl)
+              if (in_list(s0 == 0 ? lc.ml : lc.nl, l)) grp.push_back(l);
+            kin = pick16(grp);
+            if (!kin.empty()) side_of[lead] = s0;
+          }
         }
       }
       if (!kin.empty()) {
@@ -632,7 +658,8 @@ int compile(Plan& P, const tnx_plan_desc* D) {
             all_m = all_m && in_list(cv.ml, l);
             all_n = all_n && in_list(cv.nl, l);
           }
-          if (side == lead) cv.swap = !lead_rows_m;
+          if (side_of[side] == 0 && all_m) cv.swap = false;
+          else if (side_of[side] == 1 && all_n) cv.swap = true;
           else if (all_m) cv.swap = false;
           else if (all_n) cv.swap = true;
         }
@@ -656,6 +683,29 @@ int compile(Plan& P, const tnx_plan_desc* D) {
         if (tc.arena == AR_WORK && tc.block >= 0) P.blocks[ph][tc.block].bytes = kAlign;
         tc.fused = true;
       }
+    }
+  }
+  if (getenv("TNX_DEBUG_PLAN")) {
+    for (auto& v : P.V) {
+      if (v.kind != VK_GEMM) continue;
+      std::string info;
+      if (v.direct_parent >= 0) {
+        const Vertex& pv = P.V[v.direct_parent - P.n];
+        std::vector<int> dst;
+        plane_order(P, pv, v.direct_side, dst);
+        std::vector<int64_t> pst(P.L, 0);
+        int64_t acc = 1;
+        for (int i = (int)dst.size() - 1; i >= 0; --i) { pst[dst[i]] = acc; acc *= P.dims[dst[i]]; }
+        const std::vector<int>& f1 = v.swap ? v.nl : v.ml;
+        const std::vector<int>& f2 = v.swap ? v.ml : v.nl;
+        info = " rows_inner_strides=";
+        for (int i = std::max(0, (int)f1.size() - 6); i < (int)f1.size(); ++i) info += std::to_string(pst[f1[i]]) + ",";
+        info += " cols_inner_strides=";
+        for (int i = std::max(0, (int)f2.size() - 6); i < (int)f2.size(); ++i) info += std::to_string(pst[f2[i]]) + ",";
+      }
+      fprintf(stderr, "gemm v=%d M=%lld N=%lld K=%lld swap=%d splits=%d parent=%d side=%d%s\n", v.ssa,
+              (long long)v.M, (long long)v.N, (long long)v.K, (int)v.swap, v.splits, v.direct_parent,
+              v.direct_side, info.c_str());
     }
   }
   P.persist_bytes = std::max<int64_t>(persist_off, kAlign);
