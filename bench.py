@@ -239,6 +239,7 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=90.0)
     ap.add_argument("--profile-out", default=None)
     ap.add_argument("--no-tf32-probe", action="store_true")
+    ap.add_argument("--no-direct", action="store_true", help="disable GEMM->GEMM operand-plane fusion")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -266,7 +267,8 @@ def main():
     from paper_2002_01935_b200.distributed import slice_range, allreduce_complex
     t_setup = time.perf_counter()
     tn, tree, ss, meta = workload(args)
-    plan = SlicedPlan(tn, tree, ss, device=local, precision=args.precision)
+    plan = SlicedPlan(tn, tree, ss, device=local, precision=args.precision,
+                      direct_planes=not args.no_direct)
     plan.bind()
     setup_s = time.perf_counter() - t_setup
     st = plan.stats()
