@@ -107,7 +107,8 @@ typedef struct {
 /* Per internal vertex description (introspection / tests). */
 typedef struct {
   int32_t ssa;               /* vertex id n+k */
-  int32_t kind;              /* 0 SIMT thread/out, 1 SIMT warp/out, 2 SIMT split, 3 GEMM */
+  int32_t kind;              /* 0 SIMT thread/out, 1 SIMT warp/out, 2 SIMT split, 3 GEMM,
+                                4 full contraction (permute + streaming dot) */
   int32_t hoisted;           /* computed once per bind */
   int32_t rank;              /* rank of the result */
   int64_t m, n, k, batch;    /* GEMM-view extents */

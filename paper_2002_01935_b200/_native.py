@@ -18,7 +18,7 @@ DTYPE_C128, DTYPE_C64 = 0, 1
 LOC_HOST, LOC_DEVICE = 0, 1
 FLAG_NO_GRAPH, FLAG_NO_HOIST, FLAG_NO_TILED_PACK, FLAG_NO_DIRECT = 1, 2, 4, 8
 
-KIND_NAMES = {0: "simt_thread", 1: "simt_warp", 2: "simt_split", 3: "gemm_tc"}
+KIND_NAMES = {0: "simt_thread", 1: "simt_warp", 2: "simt_split", 3: "gemm_tc", 4: "dot"}
 
 
 class PlanDesc(C.Structure):

@@ -382,6 +382,55 @@ cudaError_t launch_perm(const PermParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ dot
+__global__ void __launch_bounds__(256) dot_kernel(const DotParams p) {
+  const int64_t n2 = p.n >> 1;  // complex pairs (16 B)
+  const float4* x4 = reinterpret_cast<const float4*>(p.x);
+  const float4* y4 = reinterpret_cast<const float4*>(p.y);
+  float re = 0.f, im = 0.f;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
+    const float4 a = x4[i], b = y4[i];
+    re = fmaf(a.x, b.x, re);
+    re = fmaf(-a.y, b.y, re);
+    im = fmaf(a.x, b.y, im);
+    im = fmaf(a.y, b.x, im);
+    re = fmaf(a.z, b.z, re);
+    re = fmaf(-a.w, b.w, re);
+    im = fmaf(a.z, b.w, im);
+    im = fmaf(a.w, b.z, im);
+  }
+  if ((p.n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const float2 a = p.x[p.n - 1], b = p.y[p.n - 1];
+    re += a.x * b.x - a.y * b.y;
+    im += a.x * b.y + a.y * b.x;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    re += __shfl_xor_sync(0xffffffffu, re, off);
+    im += __shfl_xor_sync(0xffffffffu, im, off);
+  }
+  __shared__ float2 red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = make_float2(re, im);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float2 v = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      v.x += red[w].x;
+      v.y += red[w].y;
+    }
+    p.partial[blockIdx.x] = v;
+  }
+}
+
+cudaError_t launch_dot(const DotParams& p, cudaStream_t st) {
+  dot_kernel<<<p.nblocks, 256, 0, st>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  simt_finalize_kernel<<<1, 128, 0, st>>>(p.partial, p.z, 1, p.nblocks);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ accumulate
 __global__ void accum_kernel(const AccumParams p) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;

@@ -100,7 +100,7 @@ struct TensorLoc {
   bool fused = false;        // never materialised (written as parent operand planes)
 };
 
-enum VKind { VK_SIMT_T = 0, VK_SIMT_W = 1, VK_SIMT_S = 2, VK_GEMM = 3 };
+enum VKind { VK_SIMT_T = 0, VK_SIMT_W = 1, VK_SIMT_S = 2, VK_GEMM = 3, VK_DOT = 4 };
 
 struct Vertex {
   int ssa = 0, a = 0, b = 0;
@@ -111,7 +111,7 @@ struct Vertex {
   int64_t B = 1, M = 1, N = 1, K = 1, kp = 0, sum_size = 1;
   int nsplit = 0;
   int64_t chunk = 0;
-  int blk_apl = -1, blk_bpl = -1, blk_part = -1;
+  int blk_apl = -1, blk_bpl = -1, blk_part = -1, blk_tmp = -1;
   int splits = 1;
   bool swap = false;  // GEMM A operand taken from y (larger row count)
   int direct_parent = -1;           // GEMM writes the parent's operand planes
@@ -120,7 +120,7 @@ struct Vertex {
   int64_t tab_off = -1;  // element offset in the sum-table buffer
 };
 
-enum LaunchType { L_GATHER, L_SIMT, L_PACK, L_GEMM, L_ACCUM, L_PERM };
+enum LaunchType { L_GATHER, L_SIMT, L_PACK, L_GEMM, L_ACCUM, L_PERM, L_DOT };
 struct Launch {
   int type;
   int idx;
@@ -178,6 +178,7 @@ struct Plan {
   std::vector<SimtParams> simt;
   std::vector<PackParams> packs;
   std::vector<PermParams> perms;
+  std::vector<DotParams> dots;
   std::vector<GemmPlan> gemms;
   AccumParams accum{};
   std::vector<float2> staging;
@@ -499,9 +500,11 @@ int compile(Plan& P, const tnx_plan_desc* D) {
     v.K = P.prod(v.cl);
     v.sum_size = v.K * P.prod(v.dxl) * P.prod(v.dyl);
     TensorLoc& z = P.T[v.ssa];
+    // tensor cores for GEMM-shaped vertices; small K (padded to 16) still
+    // goes there when the output is large (SIMT would be output-bound)
     const bool gemm = P.precision == TNX_PREC_3XTF32 && v.dxl.empty() && v.dyl.empty() &&
-                      v.M >= 128 && v.N >= 128 && v.K >= 16 &&
-                      (double)v.macs >= P.gemm_min_macs;
+                      v.M >= 128 && v.N >= 128 &&
+                      (v.K >= 16 ? (double)v.macs >= P.gemm_min_macs : v.M * v.N >= (int64_t(1) << 20));
     if (gemm) {
       v.kind = VK_GEMM;
       // A takes the operand with more rows (output rows = A rows)
@@ -519,7 +522,9 @@ int compile(Plan& P, const tnx_plan_desc* D) {
         if (keep[l] && !inx[l]) z.labels.push_back(l);
       const int64_t out = P.prod(z.labels);
       const int64_t par = 148 * 2048;
-      if (v.sum_size <= 64 || out >= par / 2) v.kind = VK_SIMT_T;
+      if (out == 1 && v.dxl.empty() && v.dyl.empty() && v.bl.empty() && v.sum_size >= (1 << 16))
+        v.kind = VK_DOT;  // full contraction: permute y to x's layout + streaming dot
+      else if (v.sum_size <= 64 || out >= par / 2) v.kind = VK_SIMT_T;
       else if (out * 32 >= par / 2) v.kind = VK_SIMT_W;
       else {
         v.kind = VK_SIMT_S;
@@ -543,6 +548,10 @@ int compile(Plan& P, const tnx_plan_desc* D) {
       z.phase = ph;
       int last = v.hoisted ? (par >= 0 ? step[par] : st) : consumer_step(v.ssa);
       z.block = add_block(ph, z.size * 8, st, last);
+    }
+    if (v.kind == VK_DOT) {
+      if (x.labels != y.labels) v.blk_tmp = add_block(ph, 8 * y.size, st, st);
+      P.max_partial = std::max<int64_t>(P.max_partial, 148 * 4);
     }
     if (v.kind == VK_GEMM) {
       const int64_t ra = v.swap ? v.N : v.M, rb = v.swap ? v.M : v.N;
@@ -825,6 +834,9 @@ int run_launches(Plan& P, const std::vector<Launch>& ls, cudaStream_t st, int st
       case L_PERM:
         e = launch_perm(P.perms[L.idx], st);
         break;
+      case L_DOT:
+        e = launch_dot(P.dots[L.idx], st);
+        break;
       case L_GEMM:
         e = launch_gemm(P.gemms[L.idx], st);
         break;
@@ -846,6 +858,7 @@ int lower(Plan& P) {
   P.simt.clear();
   P.packs.clear();
   P.perms.clear();
+  P.dots.clear();
   P.ptabs.clear();
   P.gemms.clear();
   P.hoist_launches.clear();
@@ -946,6 +959,31 @@ int lower(Plan& P) {
         }
         P.gemms.push_back(g);
         out.push_back({L_GEMM, (int)P.gemms.size() - 1, v.ssa});
+      } else if (v.kind == VK_DOT) {
+        const float2* yp = P.ptr(y);
+        if (v.blk_tmp >= 0) {
+          PermParams pp;
+          int64_t toff = 0;
+          float2* tmp = reinterpret_cast<float2*>(P.block_ptr(phase, v.blk_tmp));
+          if (!build_perm(P, y, x.labels, 0, pp, toff, err))
+            return fail(TNX_ERR_INVALID, "vertex " + std::to_string(v.ssa) + ": dot permute: " + err);
+          pp.src = yp;
+          pp.dst = tmp;
+          if (y.arena == AR_POOL && (y.offset & 1)) pp.vec = 0;
+          pp.tab = reinterpret_cast<const int32_t*>(toff);
+          P.perms.push_back(pp);
+          out.push_back({L_PERM, (int)P.perms.size() - 1, v.ssa});
+          yp = tmp;
+        }
+        DotParams dp{};
+        dp.x = P.ptr(x);
+        dp.y = yp;
+        dp.z = P.ptr(z);
+        dp.partial = P.partial;
+        dp.n = x.size;
+        dp.nblocks = 148 * 4;
+        P.dots.push_back(dp);
+        out.push_back({L_DOT, (int)P.dots.size() - 1, v.ssa});
       } else {
         SimtParams s{};
         std::vector<int> sum = v.cl;
@@ -992,7 +1030,7 @@ void build_tables(Plan& P) {
   P.tables.clear();
   for (auto& v : P.V) {
     v.tab_off = -1;
-    if (v.kind == VK_GEMM || v.kind == VK_SIMT_S || v.sum_size > 4096) continue;
+    if (v.kind == VK_GEMM || v.kind == VK_SIMT_S || v.kind == VK_DOT || v.sum_size > 4096) continue;
     const TensorLoc& x = P.T[v.a];
     const TensorLoc& y = P.T[v.b];
     std::vector<int> sum = v.cl;
@@ -1238,7 +1276,7 @@ int tnx_stats_get(void* plan, tnx_stats* s) {
       launches += (P.V[k].splits > 1 ? 4 : 3) - (int)P.V[k].side_direct[0] - (int)P.V[k].side_direct[1];
     } else {
       ++ns;
-      launches += P.V[k].kind == VK_SIMT_S ? 2 : 1;
+      launches += P.V[k].kind == VK_SIMT_S ? 2 : P.V[k].kind == VK_DOT ? (P.V[k].blk_tmp >= 0 ? 3 : 2) : 1;
     }
   }
   s->num_gemm = ng;
@@ -1325,8 +1363,8 @@ int tnx_profile_slice(void* plan, uint64_t s, int32_t* types, int32_t* vertices,
   int m = std::min(done, (int)max_launches);
   for (int i = 0; i < m; ++i) {
     const Launch& L = P.slice_launches[i];
-    types[i] = L.type == L_GATHER ? 0 : L.type == L_SIMT ? 1 : (L.type == L_PACK || L.type == L_PERM) ? 2
-             : L.type == L_GEMM ? 3 : 4;
+    types[i] = L.type == L_GATHER ? 0 : (L.type == L_SIMT || L.type == L_DOT) ? 1
+             : (L.type == L_PACK || L.type == L_PERM) ? 2 : L.type == L_GEMM ? 3 : 4;
     vertices[i] = L.vertex;
     float t = 0.f;
     TNX_CUDA(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));

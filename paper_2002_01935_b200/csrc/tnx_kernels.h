@@ -76,6 +76,18 @@ struct PermParams {
   int32_t pad;
 };
 
+// Full contraction of two tensors in the same layout: z = sum_i x[i] y[i]
+// (block partials in FP32, finalised in FP64).
+struct DotParams {
+  const float2* x;
+  const float2* y;
+  float2* z;
+  float2* partial;
+  int64_t n;
+  int32_t nblocks;
+  int32_t pad;
+};
+
 constexpr int kMaxLeafRank = 16;
 struct GatherJob {
   int64_t src;            // element offset in the leaf pool
@@ -107,6 +119,7 @@ cudaError_t launch_gather(const GatherJob* jobs, int njobs, const float2* leaf_p
 cudaError_t launch_simt(const SimtParams& p, cudaStream_t st);
 cudaError_t launch_pack(const PackParams& p, cudaStream_t st);
 cudaError_t launch_perm(const PermParams& p, cudaStream_t st);
+cudaError_t launch_dot(const DotParams& p, cudaStream_t st);
 cudaError_t launch_accum(const AccumParams& p, cudaStream_t st);
 cudaError_t launch_set_counter(unsigned long long* counter, unsigned long long v, cudaStream_t st);
 cudaError_t launch_convert_c128(const double2* src, float2* dst, int64_t n, cudaStream_t st);
