@@ -11,4 +11,4 @@ timeout 900 python bench.py > $O/bench_default.log 2>$O/bench_default.err; echo 
 timeout 600 python bench.py --impl reference --steps 2 --warmup 0 --ref-budget 45 > $O/bench_reference.log 2>$O/bench_reference.err; echo "ref rc=$?"
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-tf32-probe"
 $CMD > $O/plain_launch.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $CMD > $O/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
-python tools/run_gemm.py 8192 8192 4096 1 2 > $O/plain_gemm.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:gemm_c64 -c 1 -o $O/prof_gemm_r1 python tools/run_gemm.py 8192 8192 4096 1 1 > $O/ncu_gemm.log 2>&1; echo "ncu gemm rc=$?"
+python tools/run_gemm.py 8192 8192 4096 1 2 > $O/plain_gemm.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:gemm_c64 -c 1 -o $O/prof_gemm_full python tools/run_gemm.py 8192 8192 4096 1 1 > $O/ncu_gemm.log 2>&1; echo "ncu gemm rc=$?"
