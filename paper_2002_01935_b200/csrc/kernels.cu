@@ -226,6 +226,83 @@ cudaError_t launch_simt(const SimtParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ batched simt
+__global__ void __launch_bounds__(256) simt_batch_kernel(const SimtParams* __restrict__ jobs,
+                                                         const int32_t* __restrict__ start, int njobs) {
+  // locate this block's job (binary search over the block prefix)
+  int lo = 0, hi = njobs - 1;
+  const int b = blockIdx.x;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (start[mid] <= b) lo = mid;
+    else hi = mid - 1;
+  }
+  const SimtParams& p = jobs[lo];
+  const int lb = b - start[lo];
+  const int nb = start[lo + 1] - start[lo];
+  if (p.mode == SIMT_THREAD) {
+    for (int64_t o = (int64_t)lb * blockDim.x + threadIdx.x; o < p.out_size; o += (int64_t)nb * blockDim.x) {
+      int64_t ox = 0, oy = 0;
+      decode2(p.out, o, ox, oy);
+      float2 acc = make_float2(0.f, 0.f);
+      if (p.sum_tab) {
+        for (int64_t j = 0; j < p.sum_size; ++j) {
+          const Int2Off t = p.sum_tab[j];
+          cfma(acc, p.x[ox + t.x], p.y[oy + t.y]);
+        }
+      } else {
+        for (int64_t j = 0; j < p.sum_size; ++j) {
+          int64_t sx = ox, sy = oy;
+          decode2(p.sum, j, sx, sy);
+          cfma(acc, p.x[sx], p.y[sy]);
+        }
+      }
+      p.z[o] = acc;
+    }
+  } else {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)lb * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)nb * blockDim.x) >> 5;
+    for (int64_t o = w0; o < p.out_size; o += nw) {
+      int64_t ox = 0, oy = 0;
+      decode2(p.out, o, ox, oy);
+      float2 acc = make_float2(0.f, 0.f);
+      for (int64_t j = lane; j < p.sum_size; j += 32) {
+        int64_t sx = ox, sy = oy;
+        if (p.sum_tab) {
+          const Int2Off t = p.sum_tab[j];
+          sx += t.x;
+          sy += t.y;
+        } else {
+          decode2(p.sum, j, sx, sy);
+        }
+        cfma(acc, p.x[sx], p.y[sy]);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+      }
+      if (lane == 0) p.z[o] = acc;
+    }
+  }
+}
+
+int simt_blocks(const SimtParams& p) {
+  const int64_t work = p.mode == SIMT_THREAD ? p.out_size : p.out_size * 32;
+  int64_t b = (work + 255) / 256;
+  if (b < 1) b = 1;
+  if (b > 148 * 16) b = 148 * 16;
+  return (int)b;
+}
+
+cudaError_t launch_simt_batch(const SimtParams* jobs, const int32_t* block_start, int njobs,
+                              int total_blocks, cudaStream_t st) {
+  if (njobs == 0) return cudaSuccess;
+  simt_batch_kernel<<<total_blocks, 256, 0, st>>>(jobs, block_start, njobs);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ pack
 __global__ void __launch_bounds__(256) pack_kernel(const PackParams p) {
   // destination planes are K-blocked: offset(r, k) = ((k / 16) * rows + r) * 16 + k % 16

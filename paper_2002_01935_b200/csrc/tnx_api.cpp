@@ -120,7 +120,7 @@ struct Vertex {
   int64_t tab_off = -1;  // element offset in the sum-table buffer
 };
 
-enum LaunchType { L_GATHER, L_SIMT, L_PACK, L_GEMM, L_ACCUM, L_PERM, L_DOT };
+enum LaunchType { L_GATHER, L_SIMT, L_PACK, L_GEMM, L_ACCUM, L_PERM, L_DOT, L_SIMTB };
 struct Launch {
   int type;
   int idx;
@@ -179,6 +179,17 @@ struct Plan {
   std::vector<PackParams> packs;
   std::vector<PermParams> perms;
   std::vector<DotParams> dots;
+  struct SimtBatch {
+    int64_t job_off = 0, start_off = 0;
+    int njobs = 0, total_blocks = 0;
+    std::vector<int> vertices;
+  };
+  std::vector<SimtBatch> batches;
+  std::vector<SimtParams> bjobs;   // all batched jobs (device copy d_bjobs)
+  std::vector<int32_t> bstarts;    // per batch: njobs + 1 block prefixes
+  SimtParams* d_bjobs = nullptr;
+  int32_t* d_bstarts = nullptr;
+  std::vector<int> level;          // slice-phase dependency level per vertex index
   std::vector<GemmPlan> gemms;
   AccumParams accum{};
   std::vector<float2> staging;
@@ -189,7 +200,7 @@ struct Plan {
     if (graph) cudaGraphDestroy(graph);
     gexec = nullptr;
     graph = nullptr;
-    void* ptrs[] = {pool, work, persist, partial, d_tabs, d_jobs, acc, comp, counter, d_ptabs};
+    void* ptrs[] = {pool, work, persist, partial, d_tabs, d_jobs, acc, comp, counter, d_ptabs, d_bjobs, d_bstarts};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     pool = nullptr;
@@ -197,6 +208,8 @@ struct Plan {
     partial = nullptr;
     d_tabs = nullptr;
     d_ptabs = nullptr;
+    d_bjobs = nullptr;
+    d_bstarts = nullptr;
     d_jobs = nullptr;
     acc = comp = nullptr;
     counter = nullptr;
@@ -452,8 +465,23 @@ int compile(Plan& P, const tnx_plan_desc* D) {
     return TNX_OK;
   }
 
-  // execution order
-  for (int k = 0; k < P.n - 1; ++k) (P.V[k].hoisted ? P.hoist_order : P.slice_order).push_back(k);
+  // execution order: hoisted vertices in SSA order; slice-dependent vertices
+  // by dependency level (all vertices of a level form one step: independent,
+  // batched into shared launches, and disjoint in memory by construction)
+  P.level.assign(P.n - 1, 0);
+  for (int k = 0; k < P.n - 1; ++k) {
+    if (P.V[k].hoisted) {
+      P.hoist_order.push_back(k);
+      continue;
+    }
+    int lv = 0;
+    for (int c : {P.V[k].a, P.V[k].b})
+      if (c >= P.n && !P.V[c - P.n].hoisted) lv = std::max(lv, P.level[c - P.n]);
+    P.level[k] = lv + 1;
+    P.slice_order.push_back(k);
+  }
+  std::stable_sort(P.slice_order.begin(), P.slice_order.end(),
+                   [&](int a, int b) { return P.level[a] < P.level[b]; });
 
   // per-vertex lowering + memory blocks
   auto add_block = [&](int phase, int64_t bytes, int first, int last) {
@@ -467,8 +495,12 @@ int compile(Plan& P, const tnx_plan_desc* D) {
   // step index of each vertex within its phase (slice phase: gather = 0)
   std::vector<int> step(nv, 0);
   for (size_t i = 0; i < P.hoist_order.size(); ++i) step[P.n + P.hoist_order[i]] = (int)i;
-  for (size_t i = 0; i < P.slice_order.size(); ++i) step[P.n + P.slice_order[i]] = (int)i + 1;
-  const int accum_step = (int)P.slice_order.size() + 1;
+  int max_level = 0;
+  for (int k : P.slice_order) {
+    step[P.n + k] = P.level[k];
+    max_level = std::max(max_level, P.level[k]);
+  }
+  const int accum_step = max_level + 1;
   const int root = P.n > 1 ? 2 * P.n - 2 : 0;
   auto consumer_step = [&](int v) {
     int p = P.parent[v];
@@ -837,6 +869,15 @@ int run_launches(Plan& P, const std::vector<Launch>& ls, cudaStream_t st, int st
       case L_DOT:
         e = launch_dot(P.dots[L.idx], st);
         break;
+      case L_SIMTB: {
+        const Plan::SimtBatch& bt = P.batches[L.idx];
+        e = launch_simt_batch(P.d_bjobs + bt.job_off, P.d_bstarts + bt.start_off, bt.njobs,
+                              bt.total_blocks, st);
+        if (e == cudaSuccess && stop_vertex >= 0 &&
+            std::find(bt.vertices.begin(), bt.vertices.end(), stop_vertex) != bt.vertices.end())
+          return TNX_OK;
+        break;
+      }
       case L_GEMM:
         e = launch_gemm(P.gemms[L.idx], st);
         break;
@@ -864,11 +905,19 @@ int lower(Plan& P) {
   P.hoist_launches.clear();
   P.slice_launches.clear();
   if (!P.gather_leaves.empty()) P.slice_launches.push_back({L_GATHER, 0, -1});
+  P.batches.clear();
+  P.bjobs.clear();
+  P.bstarts.clear();
   for (int phase = 0; phase < 2; ++phase) {
     const std::vector<int>& order = phase == 0 ? P.hoist_order : P.slice_order;
     std::vector<Launch>& out = phase == 0 ? P.hoist_launches : P.slice_launches;
+    int open_batch = -1, batch_level = -1;
     for (int k : order) {
       Vertex& v = P.V[k];
+      if (phase == 1 && P.level[k] != batch_level) {
+        open_batch = -1;
+        batch_level = P.level[k];
+      }
       const TensorLoc& x = P.T[v.a];
       const TensorLoc& y = P.T[v.b];
       const TensorLoc& z = P.T[v.ssa];
@@ -1001,6 +1050,20 @@ int lower(Plan& P) {
         s.chunk = v.chunk;
         s.partial = P.partial;
         s.sum_tab = v.tab_off >= 0 ? P.d_tabs + v.tab_off : nullptr;
+        if (phase == 1 && (v.kind == VK_SIMT_T || v.kind == VK_SIMT_W)) {
+          // one launch per dependency level for all its small contractions
+          if (open_batch < 0) {
+            P.batches.push_back(Plan::SimtBatch());
+            open_batch = (int)P.batches.size() - 1;
+            P.batches[open_batch].job_off = (int64_t)P.bjobs.size();
+            out.push_back({L_SIMTB, open_batch, -1});
+          }
+          Plan::SimtBatch& bt = P.batches[open_batch];
+          bt.vertices.push_back(v.ssa);
+          bt.njobs++;
+          P.bjobs.push_back(s);
+          continue;
+        }
         P.simt.push_back(s);
         out.push_back({L_SIMT, (int)P.simt.size() - 1, v.ssa});
       }
@@ -1155,6 +1218,23 @@ int tnx_bind_leaves(void* plan, const void* const* leaf_data, int32_t dtype, int
     }
     int rc = lower(P);
     if (rc) return rc;
+    for (auto& bt : P.batches) {
+      bt.start_off = (int64_t)P.bstarts.size();
+      int acc_blocks = 0;
+      for (int j = 0; j < bt.njobs; ++j) {
+        P.bstarts.push_back(acc_blocks);
+        acc_blocks += simt_blocks(P.bjobs[bt.job_off + j]);
+      }
+      P.bstarts.push_back(acc_blocks);
+      bt.total_blocks = acc_blocks;
+    }
+    if (!P.bjobs.empty()) {
+      TNX_CUDA(cudaMalloc(&P.d_bjobs, P.bjobs.size() * sizeof(SimtParams)));
+      TNX_CUDA(cudaMemcpy(P.d_bjobs, P.bjobs.data(), P.bjobs.size() * sizeof(SimtParams), cudaMemcpyHostToDevice));
+      TNX_CUDA(cudaMalloc(&P.d_bstarts, P.bstarts.size() * sizeof(int32_t)));
+      TNX_CUDA(cudaMemcpy(P.d_bstarts, P.bstarts.data(), P.bstarts.size() * sizeof(int32_t),
+                          cudaMemcpyHostToDevice));
+    }
     if (!P.ptabs.empty()) {
       TNX_CUDA(cudaMalloc(&P.d_ptabs, P.ptabs.size() * sizeof(int32_t)));
       TNX_CUDA(cudaMemcpy(P.d_ptabs, P.ptabs.data(), P.ptabs.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -1281,6 +1361,14 @@ int tnx_stats_get(void* plan, tnx_stats* s) {
   }
   s->num_gemm = ng;
   s->num_simt = ns;
+  if (P.bound) {
+    launches = 0;
+    for (const Launch& L : P.slice_launches)
+      launches += (L.type == L_GEMM && P.gemms[L.idx].splits > 1) || L.type == L_DOT ||
+                          (L.type == L_SIMT && P.simt[L.idx].mode == SIMT_SPLIT)
+                      ? 2
+                      : 1;
+  }
   s->launches_per_slice = launches;
   s->out_rank = (int)P.output.size();
   s->out_elements = P.out_size;
@@ -1363,7 +1451,7 @@ int tnx_profile_slice(void* plan, uint64_t s, int32_t* types, int32_t* vertices,
   int m = std::min(done, (int)max_launches);
   for (int i = 0; i < m; ++i) {
     const Launch& L = P.slice_launches[i];
-    types[i] = L.type == L_GATHER ? 0 : (L.type == L_SIMT || L.type == L_DOT) ? 1
+    types[i] = L.type == L_GATHER ? 0 : (L.type == L_SIMT || L.type == L_DOT || L.type == L_SIMTB) ? 1
              : (L.type == L_PACK || L.type == L_PERM) ? 2 : L.type == L_GEMM ? 3 : 4;
     vertices[i] = L.vertex;
     float t = 0.f;

@@ -117,6 +117,12 @@ struct AccumParams {
 cudaError_t launch_gather(const GatherJob* jobs, int njobs, const float2* leaf_pool,
                           const unsigned long long* slice_counter, cudaStream_t st);
 cudaError_t launch_simt(const SimtParams& p, cudaStream_t st);
+// One launch for many independent thread/warp-mode SIMT contractions (one
+// dependency level of the tree): block b runs job j with
+// block_start[j] <= b < block_start[j+1].
+cudaError_t launch_simt_batch(const SimtParams* jobs, const int32_t* block_start, int njobs,
+                              int total_blocks, cudaStream_t st);
+int simt_blocks(const SimtParams& p);
 cudaError_t launch_pack(const PackParams& p, cudaStream_t st);
 cudaError_t launch_perm(const PermParams& p, cudaStream_t st);
 cudaError_t launch_dot(const DotParams& p, cudaStream_t st);

@@ -127,7 +127,10 @@ class SlicedPlan:
         return self._stats.width
 
     def stats(self):
-        s = self._stats
+        st = nat.Stats()
+        nat.check(self._lib.tnx_stats_get(self._h, C.byref(st)))
+        self._stats = st
+        s = st
         return {"op_count_per_slice": self.ops_per_slice, "d": self.d, "W_s": s.width,
                 "peak_elements": s.peak_elements, "work_arena_bytes": s.work_arena_bytes,
                 "persistent_bytes": s.persistent_bytes, "leaf_bytes": s.leaf_bytes,
