@@ -198,3 +198,65 @@ def test_direct_planes_fusion_matches_materialised():
     assert rel_err(vals[0], vals[1]) <= 2e-6
     ref, _, _ = oracle.contract_sliced(tn, tree, ss.labels, slice_ids=range(0, 8))
     assert rel_err(vals[0], ref) <= TOL
+
+
+def _two_tensor_net(xl, yl, out, seed=0):
+    rng = np.random.default_rng(seed)
+    labels = list(dict.fromkeys(list(xl) + list(yl)))
+    tab = {l: 2 for l in labels}
+    x = (rng.standard_normal((2,) * len(xl)) + 1j * rng.standard_normal((2,) * len(xl))) / 2 ** (len(xl) / 4)
+    y = (rng.standard_normal((2,) * len(yl)) + 1j * rng.standard_normal((2,) * len(yl))) / 2 ** (len(yl) / 4)
+    from paper_2002_01935_b200.tree import ContractionTree
+    tn = TensorNetwork([TensorNode(0, xl, x), TensorNode(1, yl, y)], tab, tuple(out))
+    return tn, ContractionTree((0, 1), [(0, 1)])
+
+
+def test_dot_path_permuted_layouts():
+    labels = [f"a{i}" for i in range(20)]
+    rng = np.random.default_rng(1)
+    yl = list(rng.permutation(labels))
+    tn, tree = _two_tensor_net(labels, yl, ())
+    plan = SlicedPlan(tn, tree, ()).bind()
+    assert [v["kind"] for v in plan.vertex_info()] == ["dot"]
+    plan.run()
+    got = complex(plan.result())
+    plan.close()
+    ref, _, _ = oracle.contract(tn, tree)
+    assert abs(got - ref) <= 1e-5 * max(abs(ref), 1e-3)
+
+
+def test_small_k_contraction_on_tensor_cores():
+    ml = [f"m{i}" for i in range(11)]
+    nl = [f"n{i}" for i in range(10)]
+    kl = ["k0", "k1"]
+    tn, tree = _two_tensor_net(ml + kl, kl[::-1] + nl, ml + nl)
+    plan = SlicedPlan(tn, tree, ()).bind()
+    assert [v["kind"] for v in plan.vertex_info()] == ["gemm_tc"]
+    plan.run()
+    got = plan.result()
+    plan.close()
+    ref, _, _ = oracle.contract(tn, tree)
+    assert rel_err(got, ref) <= 2e-6
+
+
+def test_contract_cli_json(tmp_path):
+    import json
+    from paper_2002_01935_b200.network import save_network
+    from paper_2002_01935_b200.tree import tree_to_path_dict
+    from paper_2002_01935_b200.contract_cli import main
+    tn = gen.grid_circuit(4, 4, 10, seed=3)
+    tree = best_greedy_tree(tn, trials=2)
+    ss = greedy_slice(tree, tn, metrics(tree, tn).width - 2, restarts=1)
+    save_network(tn, tmp_path / "n.json")
+    (tmp_path / "p.json").write_text(json.dumps(tree_to_path_dict(tree, "ssa")))
+    (tmp_path / "s.json").write_text(json.dumps(ss.to_dict()))
+    import io, contextlib
+    buf = io.StringIO()
+    with contextlib.redirect_stdout(buf):
+        rc = main([str(tmp_path / "n.json"), str(tmp_path / "p.json"), "--slices", str(tmp_path / "s.json")])
+    assert rc == 0
+    doc = json.loads(buf.getvalue())
+    ref, _, ops = oracle.contract_sliced(tn, tree, ss.labels)
+    got = complex(*doc["value"])
+    assert abs(got - ref) <= 1e-5 * abs(ref)
+    assert int(doc["op_count"]) == ops == ss.Cs
