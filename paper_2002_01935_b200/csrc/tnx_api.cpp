@@ -468,20 +468,18 @@ int compile(Plan& P, const tnx_plan_desc* D) {
   // execution order: hoisted vertices in SSA order; slice-dependent vertices
   // by dependency level (all vertices of a level form one step: independent,
   // batched into shared launches, and disjoint in memory by construction)
+  // (the hoisted phase is level-scheduled the same way within its own DAG)
   P.level.assign(P.n - 1, 0);
   for (int k = 0; k < P.n - 1; ++k) {
-    if (P.V[k].hoisted) {
-      P.hoist_order.push_back(k);
-      continue;
-    }
     int lv = 0;
     for (int c : {P.V[k].a, P.V[k].b})
-      if (c >= P.n && !P.V[c - P.n].hoisted) lv = std::max(lv, P.level[c - P.n]);
+      if (c >= P.n && P.V[c - P.n].hoisted == P.V[k].hoisted) lv = std::max(lv, P.level[c - P.n]);
     P.level[k] = lv + 1;
-    P.slice_order.push_back(k);
+    (P.V[k].hoisted ? P.hoist_order : P.slice_order).push_back(k);
   }
-  std::stable_sort(P.slice_order.begin(), P.slice_order.end(),
-                   [&](int a, int b) { return P.level[a] < P.level[b]; });
+  auto by_level = [&](int a, int b) { return P.level[a] < P.level[b]; };
+  std::stable_sort(P.hoist_order.begin(), P.hoist_order.end(), by_level);
+  std::stable_sort(P.slice_order.begin(), P.slice_order.end(), by_level);
 
   // per-vertex lowering + memory blocks
   auto add_block = [&](int phase, int64_t bytes, int first, int last) {
@@ -494,7 +492,7 @@ int compile(Plan& P, const tnx_plan_desc* D) {
   };
   // step index of each vertex within its phase (slice phase: gather = 0)
   std::vector<int> step(nv, 0);
-  for (size_t i = 0; i < P.hoist_order.size(); ++i) step[P.n + P.hoist_order[i]] = (int)i;
+  for (int k : P.hoist_order) step[P.n + k] = P.level[k] - 1;
   int max_level = 0;
   for (int k : P.slice_order) {
     step[P.n + k] = P.level[k];
@@ -914,7 +912,7 @@ int lower(Plan& P) {
     int open_batch = -1, batch_level = -1;
     for (int k : order) {
       Vertex& v = P.V[k];
-      if (phase == 1 && P.level[k] != batch_level) {
+      if (P.level[k] != batch_level) {
         open_batch = -1;
         batch_level = P.level[k];
       }
@@ -1050,7 +1048,7 @@ int lower(Plan& P) {
         s.chunk = v.chunk;
         s.partial = P.partial;
         s.sum_tab = v.tab_off >= 0 ? P.d_tabs + v.tab_off : nullptr;
-        if (phase == 1 && (v.kind == VK_SIMT_T || v.kind == VK_SIMT_W)) {
+        if (v.kind == VK_SIMT_T || v.kind == VK_SIMT_W) {
           // one launch per dependency level for all its small contractions
           if (open_batch < 0) {
             P.batches.push_back(Plan::SimtBatch());

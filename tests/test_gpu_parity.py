@@ -260,3 +260,31 @@ def test_contract_cli_json(tmp_path):
     got = complex(*doc["value"])
     assert abs(got - ref) <= 1e-5 * abs(ref)
     assert int(doc["op_count"]) == ops == ss.Cs
+
+
+def test_batched_hyperedge_gemm():
+    """Shared labels kept at the vertex (hyperedge / batch dims, dense.py:64-66)
+    on the tensor-core path: z[b, m, n] = sum_k x[b, m, k] y[b, n, k]."""
+    bl = ["b0", "b1"]
+    ml = [f"m{i}" for i in range(8)]
+    nl = [f"n{i}" for i in range(8)]
+    kl = [f"k{i}" for i in range(6)]
+    # batch labels also appear on a third (tiny) node so they are hyperedges kept at the pair
+    rng = np.random.default_rng(5)
+    xl, yl = bl + ml + kl, kl[::-1] + nl + bl[::-1]
+    tab = {l: 2 for l in bl + ml + nl + kl}
+    x = (rng.standard_normal((2,) * len(xl)) + 1j * rng.standard_normal((2,) * len(xl))) / 8
+    y = (rng.standard_normal((2,) * len(yl)) + 1j * rng.standard_normal((2,) * len(yl))) / 8
+    w = rng.standard_normal((2, 2)) + 0j
+    from paper_2002_01935_b200.tree import ContractionTree
+    tn = TensorNetwork([TensorNode(0, xl, x), TensorNode(1, yl, y), TensorNode(2, bl, w)], tab,
+                       tuple(ml + nl))
+    tree = ContractionTree((0, 1, 2), [(0, 1), (3, 2)])
+    plan = SlicedPlan(tn, tree, ()).bind()
+    info = plan.vertex_info()
+    assert info[0]["kind"] == "gemm_tc" and info[0]["batch"] == 4
+    plan.run()
+    got = plan.result()
+    plan.close()
+    ref, _, _ = oracle.contract(tn, tree)
+    assert rel_err(got, ref) <= 2e-6
