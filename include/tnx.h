@@ -57,8 +57,12 @@ enum {
   TNX_FLAG_NO_GRAPH = 1u << 0,   /* launch per-slice steps directly (debug) */
   TNX_FLAG_NO_HOIST = 1u << 1,   /* recompute slice-invariant subtrees per slice */
   TNX_FLAG_NO_TILED_PACK = 1u << 2, /* GEMM operands via the gather pack kernel only */
-  TNX_FLAG_NO_DIRECT = 1u << 3      /* no GEMM->GEMM operand-plane fusion (every
+  TNX_FLAG_NO_DIRECT = 1u << 3,     /* no GEMM->GEMM operand-plane fusion (every
                                        intermediate materialised; debug dumps) */
+  TNX_FLAG_STRIP_EXPONENT = 1u << 4 /* every intermediate rescaled to unit
+                                       max-abs (exact powers of two), exponents
+                                       tracked on device; read with
+                                       tnx_partial_result_exp */
 };
 
 /*
@@ -138,6 +142,9 @@ int tnx_reset_accumulator(void* plan, void* stream);
 /* Copy the accumulator (complex128 interleaved, tn.output order) to host;
  * synchronises `stream`.  out_elems must equal stats.out_elements. */
 int tnx_partial_result(void* plan, double* out, int64_t out_elems, void* stream);
+
+/* strip_exponent plans: per output element value = out * 2^exp2. */
+int tnx_partial_result_exp(void* plan, double* out, int64_t* exp2, int64_t out_elems, void* stream);
 
 int tnx_stats_get(void* plan, tnx_stats* out);
 int tnx_vertex_info_get(void* plan, int32_t index, tnx_vertex_info* out);

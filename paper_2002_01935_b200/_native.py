@@ -16,7 +16,7 @@ TNX_OK, TNX_ERR_INVALID, TNX_ERR_DATA, TNX_ERR_CUDA, TNX_ERR_OOM, TNX_ERR_NUMERI
 PREC_FP32, PREC_3XTF32 = 0, 1
 DTYPE_C128, DTYPE_C64 = 0, 1
 LOC_HOST, LOC_DEVICE = 0, 1
-FLAG_NO_GRAPH, FLAG_NO_HOIST, FLAG_NO_TILED_PACK, FLAG_NO_DIRECT = 1, 2, 4, 8
+FLAG_NO_GRAPH, FLAG_NO_HOIST, FLAG_NO_TILED_PACK, FLAG_NO_DIRECT, FLAG_STRIP_EXPONENT = 1, 2, 4, 8, 16
 
 KIND_NAMES = {0: "simt_thread", 1: "simt_warp", 2: "simt_split", 3: "gemm_tc", 4: "dot"}
 
@@ -65,6 +65,8 @@ SIGNATURES = {
     "tnx_run_slices": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]),
     "tnx_reset_accumulator": (C.c_int, [C.c_void_p, C.c_void_p]),
     "tnx_partial_result": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_int64, C.c_void_p]),
+    "tnx_partial_result_exp": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int64,
+                                         C.c_void_p]),
     "tnx_stats_get": (C.c_int, [C.c_void_p, C.POINTER(Stats)]),
     "tnx_vertex_info_get": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(VertexInfo)]),
     "tnx_debug_vertex": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int32, C.POINTER(C.c_float), C.c_int64,

@@ -523,6 +523,28 @@ __global__ void accum_kernel(const AccumParams p) {
       re += v.x;
       im += v.y;
     }
+    if (p.acc_exp) {
+      // exponent-tracking accumulation: acc[o] * 2^acc_exp[o] += (re, im) * 2^e
+      const long long e = *p.hoist_exp + *p.slice_exp;
+      double2 s = p.acc[o];
+      long long ae = p.acc_exp[o];
+      if (re != 0.0 || im != 0.0) {
+        if (s.x == 0.0 && s.y == 0.0) {
+          s = make_double2(re, im);
+          ae = e;
+        } else if (e > ae) {
+          const double f = ldexp(1.0, (int)max(-1100LL, ae - e));
+          s = make_double2(s.x * f + re, s.y * f + im);
+          ae = e;
+        } else {
+          const double f = ldexp(1.0, (int)max(-1100LL, e - ae));
+          s = make_double2(s.x + re * f, s.y + im * f);
+        }
+      }
+      p.acc[o] = s;
+      p.acc_exp[o] = ae;
+      continue;
+    }
     // Kahan-compensated complex128 accumulation
     double2 s = p.acc[o], c = p.comp[o];
     double yr = re - c.x, yi = im - c.y;
@@ -537,6 +559,44 @@ __global__ void accum_kernel(const AccumParams p) {
 
 cudaError_t launch_accum(const AccumParams& p, cudaStream_t st) {
   accum_kernel<<<grid_for(p.out_size, 256, 148 * 8), 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+__global__ void absmax_kernel(const float2* __restrict__ z, int64_t n, unsigned int* bits) {
+  float m = 0.f;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float2 v = z[i];
+    m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(bits, __float_as_uint(m));
+}
+
+__global__ void rescale_kernel(float2* __restrict__ z, int64_t n, const unsigned int* bits,
+                               long long* exp_acc) {
+  const float m = __uint_as_float(*bits);
+  if (!(m > 0.f) || !isfinite(m)) return;
+  int e;
+  frexpf(m, &e);  // m = f * 2^e, f in [0.5, 1)
+  if (e == 0) return;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float2 v = z[i];
+    z[i] = make_float2(ldexpf(v.x, -e), ldexpf(v.y, -e));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd((unsigned long long*)exp_acc, (unsigned long long)(long long)e);
+}
+
+cudaError_t launch_absmax(const float2* z, int64_t n, unsigned int* bits, cudaStream_t st) {
+  absmax_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(z, n, bits);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rescale(float2* z, int64_t n, const unsigned int* bits, long long* exp_acc,
+                           cudaStream_t st) {
+  rescale_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(z, n, bits, exp_acc);
   return cudaGetLastError();
 }
 

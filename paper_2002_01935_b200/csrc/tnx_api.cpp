@@ -120,7 +120,7 @@ struct Vertex {
   int64_t tab_off = -1;  // element offset in the sum-table buffer
 };
 
-enum LaunchType { L_GATHER, L_SIMT, L_PACK, L_GEMM, L_ACCUM, L_PERM, L_DOT, L_SIMTB };
+enum LaunchType { L_GATHER, L_SIMT, L_PACK, L_GEMM, L_ACCUM, L_PERM, L_DOT, L_SIMTB, L_RENORM, L_RESET };
 struct Launch {
   int type;
   int idx;
@@ -189,6 +189,11 @@ struct Plan {
   std::vector<int32_t> bstarts;    // per batch: njobs + 1 block prefixes
   SimtParams* d_bjobs = nullptr;
   int32_t* d_bstarts = nullptr;
+  // strip_exponent scratch: per-vertex abs-max bits, exponent counters
+  unsigned int* d_absmax = nullptr;
+  long long* d_exps = nullptr;     // [0] hoist exponent, [1] slice exponent
+  long long* d_acc_exp = nullptr;
+  bool strip() const { return (flags & TNX_FLAG_STRIP_EXPONENT) != 0; }
   std::vector<int> level;          // slice-phase dependency level per vertex index
   std::vector<GemmPlan> gemms;
   AccumParams accum{};
@@ -200,7 +205,8 @@ struct Plan {
     if (graph) cudaGraphDestroy(graph);
     gexec = nullptr;
     graph = nullptr;
-    void* ptrs[] = {pool, work, persist, partial, d_tabs, d_jobs, acc, comp, counter, d_ptabs, d_bjobs, d_bstarts};
+    void* ptrs[] = {pool,    work,   persist, partial, d_tabs,    d_jobs,   acc,    comp,
+                    counter, d_ptabs, d_bjobs, d_bstarts, d_absmax, d_exps, d_acc_exp};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     pool = nullptr;
@@ -210,6 +216,9 @@ struct Plan {
     d_ptabs = nullptr;
     d_bjobs = nullptr;
     d_bstarts = nullptr;
+    d_absmax = nullptr;
+    d_exps = nullptr;
+    d_acc_exp = nullptr;
     d_jobs = nullptr;
     acc = comp = nullptr;
     counter = nullptr;
@@ -601,7 +610,8 @@ int compile(Plan& P, const tnx_plan_desc* D) {
   //   * that child side becomes the child's row (A) side, and the child's rows
   //     and columns follow the parent's plane order, so the 32 lanes of an
   //     epilogue warp store consecutive floats (whole 128 B lines).
-  if (P.precision == TNX_PREC_3XTF32 && !(P.flags & TNX_FLAG_NO_DIRECT)) {
+  if (P.precision == TNX_PREC_3XTF32 && !(P.flags & TNX_FLAG_NO_DIRECT) &&
+      !(P.flags & TNX_FLAG_STRIP_EXPONENT)) {
     auto in_list = [](const std::vector<int>& v, int l) {
       return std::find(v.begin(), v.end(), l) != v.end();
     };
@@ -867,6 +877,20 @@ int run_launches(Plan& P, const std::vector<Launch>& ls, cudaStream_t st, int st
       case L_DOT:
         e = launch_dot(P.dots[L.idx], st);
         break;
+      case L_RENORM: {
+        const TensorLoc& t = P.T[L.idx];
+        unsigned int* bits = P.d_absmax + L.idx;
+        e = launch_absmax(P.ptr(t), t.size, bits, st);
+        if (e == cudaSuccess)
+          e = launch_rescale(P.ptr(t), t.size, bits, P.d_exps + (P.V[L.idx - P.n].hoisted ? 0 : 1), st);
+        break;
+      }
+      case L_RESET: {
+        const int nv = P.n > 1 ? 2 * P.n - 1 : 1;
+        e = cudaMemsetAsync(P.d_absmax, 0, nv * sizeof(unsigned int), st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(P.d_exps + L.idx, 0, sizeof(long long), st);
+        break;
+      }
       case L_SIMTB: {
         const Plan::SimtBatch& bt = P.batches[L.idx];
         e = launch_simt_batch(P.d_bjobs + bt.job_off, P.d_bstarts + bt.start_off, bt.njobs,
@@ -885,7 +909,9 @@ int run_launches(Plan& P, const std::vector<Launch>& ls, cudaStream_t st, int st
         break;
     }
     if (e != cudaSuccess) return fail(TNX_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
-    if (stop_vertex >= 0 && L.vertex == stop_vertex && L.type != L_PACK && L.type != L_PERM) break;
+    if (stop_vertex >= 0 && L.vertex == stop_vertex && L.type != L_PACK && L.type != L_PERM &&
+        L.type != L_RENORM)
+      break;
   }
   return TNX_OK;
 }
@@ -909,13 +935,19 @@ int lower(Plan& P) {
   for (int phase = 0; phase < 2; ++phase) {
     const std::vector<int>& order = phase == 0 ? P.hoist_order : P.slice_order;
     std::vector<Launch>& out = phase == 0 ? P.hoist_launches : P.slice_launches;
+    if (P.strip()) out.push_back({L_RESET, phase, -1});
     int open_batch = -1, batch_level = -1;
+    std::vector<int> pending_renorm;  // strip_exponent: batched vertices of the open level
+    size_t renorm_mark = 0;
     for (int k : order) {
       Vertex& v = P.V[k];
       if (P.level[k] != batch_level) {
+        for (int pv : pending_renorm) out.push_back({L_RENORM, pv, pv});
+        pending_renorm.clear();
         open_batch = -1;
         batch_level = P.level[k];
       }
+      renorm_mark = out.size();
       const TensorLoc& x = P.T[v.a];
       const TensorLoc& y = P.T[v.b];
       const TensorLoc& z = P.T[v.ssa];
@@ -1060,12 +1092,15 @@ int lower(Plan& P) {
           bt.vertices.push_back(v.ssa);
           bt.njobs++;
           P.bjobs.push_back(s);
+          if (P.strip()) pending_renorm.push_back(v.ssa);
           continue;
         }
         P.simt.push_back(s);
         out.push_back({L_SIMT, (int)P.simt.size() - 1, v.ssa});
       }
+      if (P.strip() && out.size() > renorm_mark) out.push_back({L_RENORM, v.ssa, v.ssa});
     }
+    for (int pv : pending_renorm) out.push_back({L_RENORM, pv, pv});
   }
   // accumulate: root -> output order
   const int root = P.n > 1 ? 2 * P.n - 2 : 0;
@@ -1082,6 +1117,11 @@ int lower(Plan& P) {
   P.accum.out_size = P.out_size;
   P.accum.extra_size = P.prod(extra);
   P.accum.slice_counter = P.counter;
+  if (P.strip()) {
+    P.accum.hoist_exp = P.d_exps;
+    P.accum.slice_exp = P.d_exps + 1;
+    P.accum.acc_exp = P.d_acc_exp;
+  }
   P.slice_launches.push_back({L_ACCUM, 0, -1});
   return TNX_OK;
 }
@@ -1177,6 +1217,13 @@ int tnx_bind_leaves(void* plan, const void* const* leaf_data, int32_t dtype, int
     TNX_CUDA(cudaMalloc(&P.acc, std::max<int64_t>(P.out_size, 1) * 16));
     TNX_CUDA(cudaMalloc(&P.comp, std::max<int64_t>(P.out_size, 1) * 16));
     TNX_CUDA(cudaMalloc(&P.counter, 8));
+    if (P.strip()) {
+      const int nvv = P.n > 1 ? 2 * P.n - 1 : 1;
+      TNX_CUDA(cudaMalloc(&P.d_absmax, nvv * sizeof(unsigned int)));
+      TNX_CUDA(cudaMalloc(&P.d_exps, 2 * sizeof(long long)));
+      TNX_CUDA(cudaMemset(P.d_exps, 0, 2 * sizeof(long long)));
+      TNX_CUDA(cudaMalloc(&P.d_acc_exp, std::max<int64_t>(P.out_size, 1) * sizeof(long long)));
+    }
     // gather jobs
     std::vector<GatherJob> jobs;
     for (int i : P.gather_leaves) {
@@ -1276,6 +1323,7 @@ int tnx_bind_leaves(void* plan, const void* const* leaf_data, int32_t dtype, int
   if (rc) return rc;
   TNX_CUDA(cudaMemsetAsync(P.acc, 0, std::max<int64_t>(P.out_size, 1) * 16, st));
   TNX_CUDA(cudaMemsetAsync(P.comp, 0, std::max<int64_t>(P.out_size, 1) * 16, st));
+  if (P.d_acc_exp) TNX_CUDA(cudaMemsetAsync(P.d_acc_exp, 0, std::max<int64_t>(P.out_size, 1) * 8, st));
   // per-slice graph
   if (!(P.flags & TNX_FLAG_NO_GRAPH) && !P.gexec) {
     cudaStream_t cs = P.own;
@@ -1319,6 +1367,7 @@ int tnx_reset_accumulator(void* plan, void* stream) {
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.own;
   TNX_CUDA(cudaMemsetAsync(P.acc, 0, std::max<int64_t>(P.out_size, 1) * 16, st));
   TNX_CUDA(cudaMemsetAsync(P.comp, 0, std::max<int64_t>(P.out_size, 1) * 16, st));
+  if (P.d_acc_exp) TNX_CUDA(cudaMemsetAsync(P.d_acc_exp, 0, std::max<int64_t>(P.out_size, 1) * 8, st));
   return TNX_OK;
 }
 
@@ -1328,6 +1377,18 @@ int tnx_partial_result(void* plan, double* out, int64_t out_elems, void* stream)
   if (out_elems != P.out_size) return fail(TNX_ERR_INVALID, "output size mismatch");
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.own;
   TNX_CUDA(cudaMemcpyAsync(out, P.acc, P.out_size * 16, cudaMemcpyDeviceToHost, st));
+  TNX_CUDA(cudaStreamSynchronize(st));
+  return TNX_OK;
+}
+
+int tnx_partial_result_exp(void* plan, double* out, int64_t* exp2, int64_t out_elems, void* stream) {
+  Plan& P = *static_cast<Plan*>(plan);
+  if (!P.bound) return fail(TNX_ERR_STATE, "not bound");
+  if (!P.strip()) return fail(TNX_ERR_STATE, "plan was not created with TNX_FLAG_STRIP_EXPONENT");
+  if (out_elems != P.out_size) return fail(TNX_ERR_INVALID, "output size mismatch");
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.own;
+  TNX_CUDA(cudaMemcpyAsync(out, P.acc, P.out_size * 16, cudaMemcpyDeviceToHost, st));
+  TNX_CUDA(cudaMemcpyAsync(exp2, P.d_acc_exp, P.out_size * 8, cudaMemcpyDeviceToHost, st));
   TNX_CUDA(cudaStreamSynchronize(st));
   return TNX_OK;
 }

@@ -102,6 +102,12 @@ struct GatherJob {
   int64_t sst[kMaxLeafRank];
 };
 
+// strip_exponent: per-vertex abs-max + exact power-of-two
+// rescale; base-2 exponents accumulate in a device counter.
+cudaError_t launch_absmax(const float2* z, int64_t n, unsigned int* bits, cudaStream_t st);
+cudaError_t launch_rescale(float2* z, int64_t n, const unsigned int* bits, long long* exp_acc,
+                           cudaStream_t st);
+
 struct AccumParams {
   IdxMap out;             // output index -> root offset (st0)
   IdxMap extra;           // extra summed labels (single-leaf tree) -> root offset
@@ -111,6 +117,11 @@ struct AccumParams {
   int64_t out_size;
   int64_t extra_size;
   unsigned long long* slice_counter;  // advanced by one after the slice
+  // strip_exponent mode: value * 2^(hoist_exp + slice_exp) accumulated as
+  // (acc, acc_exp) per element (no Kahan in this mode)
+  const long long* hoist_exp;
+  const long long* slice_exp;
+  long long* acc_exp;
 };
 
 // launchers (return cudaError_t)

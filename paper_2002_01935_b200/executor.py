@@ -57,7 +57,8 @@ class SlicedPlan:
     """
 
     def __init__(self, tn, tree, slice_set=(), device=0, precision="3xtf32", graph=True,
-                 hoist=True, gemm_min_macs=0.0, tiled_pack=True, direct_planes=True):
+                 hoist=True, gemm_min_macs=0.0, tiled_pack=True, direct_planes=True,
+                 strip_exponent=False):
         lib = nat.load()
         self.tn = tn
         self.tree = tree
@@ -91,7 +92,9 @@ class SlicedPlan:
         k = self._keep
         flags = ((0 if graph else nat.FLAG_NO_GRAPH) | (0 if hoist else nat.FLAG_NO_HOIST)
                  | (0 if tiled_pack else nat.FLAG_NO_TILED_PACK)
-                 | (0 if direct_planes else nat.FLAG_NO_DIRECT))
+                 | (0 if direct_planes else nat.FLAG_NO_DIRECT)
+                 | (nat.FLAG_STRIP_EXPONENT if strip_exponent else 0))
+        self.strip_exponent = bool(strip_exponent)
         if precision not in PRECISIONS:
             raise ValueError(f"unknown precision {precision!r}; choose from {sorted(PRECISIONS)}")
         self.precision = precision
@@ -225,6 +228,17 @@ class SlicedPlan:
         names = {0: "gather", 1: "simt", 2: "pack", 3: "gemm", 4: "accum"}
         return [(names[ty[i]], vx[i], float(ms[i])) for i in range(cnt.value)]
 
+    def result_exp(self, stream=None):
+        """strip_exponent plans: (mantissas, base-2 exponents) per element."""
+        n = int(self._stats.out_elements)
+        buf = np.zeros(2 * max(n, 1), dtype=np.float64)
+        ex = np.zeros(max(n, 1), dtype=np.int64)
+        nat.check(self._lib.tnx_partial_result_exp(self._h, buf.ctypes.data_as(C.POINTER(C.c_double)),
+                                                   ex.ctypes.data_as(C.POINTER(C.c_int64)), n,
+                                                   self._stream(stream)))
+        m = (buf[0::2] + 1j * buf[1::2])[:n].reshape(self.out_shape)
+        return m, ex[:n].reshape(self.out_shape)
+
     def synchronize(self):
         nat.check(self._lib.tnx_synchronize(self._h))
 
@@ -268,6 +282,26 @@ class SlicedPlan:
             pass
 
 
+def _combine_exp(parts, tn):
+    """Sum of mantissa * 2^e parts -> (value, exponent10) without overflow."""
+    logs = []
+    for m, e in parts:
+        m = np.asarray(m)
+        with np.errstate(divide="ignore"):
+            lm = np.where(m != 0, np.log10(np.abs(m)) + e * math.log10(2.0), -np.inf)
+        logs.append(lm)
+    top = max(float(np.max(lm)) if np.size(lm) else -np.inf for lm in logs)
+    e10 = 0 if not np.isfinite(top) else math.floor(top)
+    total = 0
+    for m, e in parts:
+        total = total + np.asarray(m) * np.power(10.0, np.asarray(e) * math.log10(2.0) - e10)
+    arr = np.asarray(total)
+    if not np.all(np.isfinite(arr)):
+        raise FloatingPointError("non-finite contraction value")
+    exp10 = e10 + tn.norm_exponent
+    return (complex(arr) if arr.ndim == 0 else arr), exp10
+
+
 def _finish(val, tn, strip_exponent):
     arr = np.asarray(val)
     if not np.all(np.isfinite(arr)):
@@ -307,7 +341,8 @@ def contract_sliced(tn, tree, slice_set=(), options=None, *, slice_ids=None, dev
     options = dict(options or {})
     strip = bool(options.get("strip_exponent", False))
     devices = list(devices)
-    plans = [SlicedPlan(tn, tree, slice_set, device=d, precision=precision, graph=graph, hoist=hoist)
+    plans = [SlicedPlan(tn, tree, slice_set, device=d, precision=precision, graph=graph, hoist=hoist,
+                        strip_exponent=strip)
              for d in devices]
     try:
         s0, s1 = _slice_range(plans[0].d, slice_ids)
@@ -323,7 +358,7 @@ def contract_sliced(tn, tree, slice_set=(), options=None, *, slice_ids=None, dev
                 p = plans[g]
                 p.bind()
                 p.run(bounds[g], bounds[g + 1])
-                parts[g] = p.result()
+                parts[g] = p.result_exp() if strip else p.result()
             except BaseException as exc:  # noqa: BLE001
                 errs[g] = exc
 
@@ -338,10 +373,13 @@ def contract_sliced(tn, tree, slice_set=(), options=None, *, slice_ids=None, dev
         for e in errs:
             if e is not None:
                 raise e
+        ops = plans[0].ops_per_slice * (s1 - s0)
+        if strip:
+            val, exp10 = _combine_exp(parts, tn)
+            return val, exp10, ops
         total = parts[0]
         for p in parts[1:]:
             total = total + p
-        ops = plans[0].ops_per_slice * (s1 - s0)
         val, exp10 = _finish(total, tn, strip)
         return val, exp10, ops
     finally:

@@ -288,3 +288,27 @@ def test_batched_hyperedge_gemm():
     plan.close()
     ref, _, _ = oracle.contract(tn, tree)
     assert rel_err(got, ref) <= 2e-6
+
+
+def test_strip_exponent_beyond_fp32_range():
+    """with strip_exponent every intermediate is renormalised
+    on device, so a network whose value is far outside FP32 range contracts
+    correctly; value * 10^exponent is invariant."""
+    tn0 = gen.random_regular(40, 3, seed=9)
+    # blow every leaf up by 1e6: value scales by 1e240 (beyond FP32 and FP64 range)
+    tn = tn0.replace(nodes=[TensorNode(nd.id, nd.indices, nd.data * 1e6) for nd in tn0.nodes])
+    tree = best_greedy_tree(tn0, trials=2)
+    S = list(tn.index_table)[:3]
+    ref0, _, _ = oracle.contract_sliced(tn0, tree, S)
+    val, e10, _ = contract_sliced(tn, tree, S, {"strip_exponent": True})
+    # compare log10 magnitudes and phases
+    lg = np.log10(abs(val)) + e10
+    lg_ref = np.log10(abs(ref0)) + 240
+    assert abs(lg - lg_ref) < 1e-5
+    assert abs(np.angle(val) - np.angle(ref0)) < 1e-4
+    # plain mode overflows -> FloatingPointError, like the SPEC's non-finite check
+    with pytest.raises(FloatingPointError):
+        contract_sliced(tn, tree, S)
+    # strip mode on an ordinary network agrees with plain mode
+    v2, e2, _ = contract_sliced(tn0, tree, S, {"strip_exponent": True})
+    assert abs(v2 * 10.0 ** e2 - ref0) <= 1e-5 * abs(ref0)
