@@ -328,17 +328,13 @@ def main():
     slices_per_s = total_slices / (ms_max / 1e3)
 
     # per-launch profile of one slice (CUDA events on the launching stream)
-    prof = plan.profile_slice(base + W)
+    prof_b = plan.profile_slice(base + W, with_bytes=True)
+    prof = [(k, v, t) for k, v, t, b in prof_b]
     info = {v["ssa"]: v for v in plan.vertex_info()}
     gemm_ms = sum(t for k, v, t in prof if k == "gemm")
     gemm_flops = sum(8 * info[v]["macs"] for k, v, t in prof if k == "gemm")
     n_gemm = sum(1 for k, v, t in prof if k == "gemm")
     slice_ms = sum(t for _, _, t in prof)
-    pack_bytes = 0
-    for k, v, t in prof:
-        if k == "pack":
-            x = info[v]
-            pack_bytes += 0  # accounted per operand below
     peaks, peak_kind = load_peaks()
     p_tf32 = measure_tf32_peak(torch) if not args.no_tf32_probe else None
     # primary roofline: the driver-measured bf16 peak -> TF32 (half rate) -> /3 split passes
@@ -349,17 +345,48 @@ def main():
         peak_src += f"; live cuBLAS TF32 8192^3 this run: {p_tf32:.1f} TFLOP/s (/3 = {p_tf32 / 3:.1f})"
     achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
     traffic = load_traffic()
+    # per-vertex roofline of the dominant contractions (top vertices covering
+    # >= 90 % of the slice's FLOPs; the north-star criterion)
+    per_v = {}
+    for k, v, t in prof:
+        if v >= 0:
+            per_v.setdefault(v, {"gemm": 0.0, "other": 0.0})
+            per_v[v]["gemm" if k == "gemm" else "other"] += t
+    fl_total = 8 * sum(x["macs"] for x in info.values())
+    dom, acc_fl = [], 0
+    for v in sorted(info, key=lambda u: -info[u]["macs"]):
+        if acc_fl >= 0.9 * fl_total or v not in per_v:
+            break
+        x = info[v]
+        fl = 8 * x["macs"]
+        t = per_v[v]["gemm"] + per_v[v]["other"]
+        dom.append({"ssa": v, "kind": x["kind"], "M": x["m"], "N": x["n"], "K": x["k"], "ms": round(t, 4),
+                    "flop_share": round(fl / fl_total, 4), "tflops": round(fl / t / 1e9, 1),
+                    "frac": round(fl / t / 1e9 / p_c, 3)})
+        acc_fl += fl
+    # HBM roofline of the memory-bound kernels (permute / pack / dot): algorithmic
+    # bytes per launch reported by the library
+    mem_ms = sum(t for k, v, t, b in prof_b if k == "pack" or (k == "simt" and b > 0))
+    mem_bytes = sum(b for k, v, t, b in prof_b if k == "pack" or (k == "simt" and b > 0))
+    hbm = {"kernels": "perm_vec/perm/pack/dot", "achieved_gbs": mem_bytes / (mem_ms / 1e3) / 1e9 if mem_ms else None,
+           "peak_gbs": peaks["hbm_gbs"], "frac": (mem_bytes / (mem_ms / 1e3) / 1e9 / peaks["hbm_gbs"]) if mem_ms else None,
+           "ms_per_slice": mem_ms}
     by_kind = {}
     for k, v, t in prof:
         by_kind[k] = by_kind.get(k, 0.0) + t
     roofline = {"bound": "tensor", "achieved": achieved, "peak": p_c, "unit": "TFLOP/s",
                 "frac": achieved / p_c if p_c else None,
                 "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+                "traffic_note": (traffic.get("kernel") + "; algorithmic bytes " +
+                                 str(traffic.get("algorithmic_bytes"))) if traffic else None,
                 "kernel": "gemm_c64_3xtf32 (tcgen05.mma.kind::tf32, 4M x 3 split passes)",
                 "peak_source": peak_src,
                 "gemm_share_of_slice": gemm_ms / slice_ms if slice_ms else None,
                 "gemm_launches_per_slice": n_gemm,
-                "time_share_ms": {k: round(t, 3) for k, t in by_kind.items()}}
+                "time_share_ms": {k: round(t, 3) for k, t in by_kind.items()},
+                "dominant_vertices": dom,
+                "dominant_min_frac": min((d["frac"] for d in dom), default=None),
+                "hbm_bound_kernels": hbm}
     if args.profile_out and rank == 0:
         with open(args.profile_out, "w") as fh:
             json.dump({"launches": prof, "vertices": list(info.values())}, fh, default=str)

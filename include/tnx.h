@@ -158,9 +158,11 @@ int tnx_debug_vertex(void* plan, uint64_t s, int32_t v, float* out_c64,
 /* Profiling: run slice s (not accumulated) launch by launch on the plan's
  * stream with CUDA events around every kernel; fills up to max_launches
  * entries (type: 0 gather, 1 simt, 2 pack, 3 gemm, 4 accum; vertex = SSA id
- * or -1; ms = event-timed duration) and returns the count in *count. */
+ * or -1; ms = event-timed duration; alg_bytes = algorithmic HBM bytes of
+ * memory-bound launches (permute/pack: 8 B read + 16 B written per element,
+ * dot: 16 B per element), 0 for compute-bound ones) and returns the count. */
 int tnx_profile_slice(void* plan, uint64_t s, int32_t* types, int32_t* vertices, float* ms,
-                      int32_t max_launches, int32_t* count);
+                      double* alg_bytes, int32_t max_launches, int32_t* count);
 
 /* Synchronise the plan's device; returns a CUDA error if one is pending. */
 int tnx_synchronize(void* plan);

@@ -73,7 +73,8 @@ SIGNATURES = {
                                    C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "tnx_synchronize": (C.c_int, [C.c_void_p]),
     "tnx_profile_slice": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
-                                    C.POINTER(C.c_float), C.c_int32, C.POINTER(C.c_int32)]),
+                                    C.POINTER(C.c_float), C.POINTER(C.c_double), C.c_int32,
+                                    C.POINTER(C.c_int32)]),
     "tnx_gemm_c64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
                                C.c_int64, C.c_int32, C.c_void_p]),
 }

@@ -1484,7 +1484,7 @@ int tnx_debug_vertex(void* plan, uint64_t s, int32_t v, float* out_c64, int64_t 
 }
 
 int tnx_profile_slice(void* plan, uint64_t s, int32_t* types, int32_t* vertices, float* ms,
-                      int32_t max_launches, int32_t* count) {
+                      double* alg_bytes, int32_t max_launches, int32_t* count) {
   Plan& P = *static_cast<Plan*>(plan);
   if (!P.bound) return fail(TNX_ERR_STATE, "not bound");
   if ((u128)s >= P.d) return fail(TNX_ERR_INVALID, "slice out of range");
@@ -1513,6 +1513,19 @@ int tnx_profile_slice(void* plan, uint64_t s, int32_t* types, int32_t* vertices,
     types[i] = L.type == L_GATHER ? 0 : (L.type == L_SIMT || L.type == L_DOT || L.type == L_SIMTB) ? 1
              : (L.type == L_PACK || L.type == L_PERM) ? 2 : L.type == L_GEMM ? 3 : 4;
     vertices[i] = L.vertex;
+    if (alg_bytes) {
+      double b = 0.0;
+      if (L.type == L_PERM) {
+        const PermParams& pp = P.perms[L.idx];
+        b = (double)pp.n_outer * pp.ts * (pp.mode == 0 ? 16.0 : 24.0);
+      } else if (L.type == L_PACK) {
+        const PackParams& pk = P.packs[L.idx];
+        b = (double)pk.rows * pk.K * 8.0 + (double)pk.rows * pk.kp * 16.0;
+      } else if (L.type == L_DOT) {
+        b = (double)P.dots[L.idx].n * 16.0;
+      }
+      alg_bytes[i] = b;
+    }
     float t = 0.f;
     TNX_CUDA(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
     ms[i] = t;

@@ -216,16 +216,19 @@ class SlicedPlan:
         val = (buf[0::2] + 1j * buf[1::2])[:n].reshape(self.out_shape)
         return val
 
-    def profile_slice(self, s=0):
+    def profile_slice(self, s=0, with_bytes=False):
         """Per-launch CUDA-event timings of one (non-accumulated) slice:
-        list of (kind, ssa vertex, ms)."""
-        n = self._stats.launches_per_slice + 4
+        list of (kind, ssa vertex, ms[, algorithmic bytes])."""
+        n = self.stats()["launches_per_slice"] + 8
         ty = (C.c_int32 * n)()
         vx = (C.c_int32 * n)()
         ms = (C.c_float * n)()
+        by = (C.c_double * n)()
         cnt = C.c_int32()
-        nat.check(self._lib.tnx_profile_slice(self._h, int(s), ty, vx, ms, n, C.byref(cnt)))
+        nat.check(self._lib.tnx_profile_slice(self._h, int(s), ty, vx, ms, by, n, C.byref(cnt)))
         names = {0: "gather", 1: "simt", 2: "pack", 3: "gemm", 4: "accum"}
+        if with_bytes:
+            return [(names[ty[i]], vx[i], float(ms[i]), float(by[i])) for i in range(cnt.value)]
         return [(names[ty[i]], vx[i], float(ms[i])) for i in range(cnt.value)]
 
     def result_exp(self, stream=None):
