@@ -312,3 +312,36 @@ def test_strip_exponent_beyond_fp32_range():
     # strip mode on an ordinary network agrees with plain mode
     v2, e2, _ = contract_sliced(tn0, tree, S, {"strip_exponent": True})
     assert abs(v2 * 10.0 ** e2 - ref0) <= 1e-5 * abs(ref0)
+
+
+@pytest.mark.parametrize("dims", [(3, 5, 3), (3, 2, 5), (7, 3, 2)])
+def test_gemm_path_odd_dims(dims):
+    """Tensor-core path with non-power-of-two label dims: ragged M/N tiles,
+    K padded to 16 (gather pack), division-based index maps, batch > 1."""
+    dm, dn, dk = dims
+    rng = np.random.default_rng(sum(dims))
+    ml = ["m0", "m1", "m2", "m3", "m4"]
+    nl = ["n0", "n1", "n2", "n3", "n4"]
+    kl = ["k0", "k1", "k2"]
+    tab = {**{l: dm for l in ml}, **{l: dn for l in nl}, **{l: dk for l in kl}, "b": 3}
+    xl, yl = ml[:3] + kl + ["b"] + ml[3:], ["b"] + nl + kl[::-1]
+    xs = tuple(tab[l] for l in xl)
+    ys = tuple(tab[l] for l in yl)
+    x = (rng.standard_normal(xs) + 1j * rng.standard_normal(xs)) / np.sqrt(np.prod(xs) ** 0.5)
+    y = (rng.standard_normal(ys) + 1j * rng.standard_normal(ys)) / np.sqrt(np.prod(ys) ** 0.5)
+    w = rng.standard_normal(3) + 0j
+    from paper_2002_01935_b200.tree import ContractionTree
+    tn = TensorNetwork([TensorNode(0, xl, x), TensorNode(1, yl, y), TensorNode(2, ["b"], w)], tab,
+                       tuple(nl[:2] + ml + nl[2:]))
+    tree = ContractionTree((0, 1, 2), [(0, 1), (3, 2)])
+    plan = SlicedPlan(tn, tree, (), gemm_min_macs=1.0).bind()
+    info = plan.vertex_info()
+    assert info[0]["kind"] == "gemm_tc", info
+    plan.run()
+    got = plan.result()
+    plan.close()
+    ref, _, _ = oracle.contract(tn, tree)
+    assert rel_err(got, ref) <= 2e-6, rel_err(got, ref)
+    # sliced on a K label and a batch label
+    val, _, _ = contract_sliced(tn, tree, ["k1", "b"])
+    assert rel_err(val, ref) <= 2e-6
