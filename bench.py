@@ -136,7 +136,15 @@ def measure_tf32_peak(torch):
 
 def workload(args):
     from paper_2002_01935_b200.harness.workloads import load_workload
-    return load_workload(args.config, ws=args.ws)
+    if args.ws == "auto":
+        import torch
+        from paper_2002_01935_b200.slicing import auto_slice
+        tn, tree, _, meta = load_workload(args.config, ws=1e9)
+        free, _total = torch.cuda.mem_get_info()
+        ss, need = auto_slice(tree, tn, free, ws_max=40)
+        meta["ws_auto"] = {"device_free_bytes": free, "plan_bytes": need}
+        return tn, tree, ss, meta
+    return load_workload(args.config, ws=None if args.ws is None else float(args.ws))
 
 
 def cpu_baseline(tn, tree, ss, slice_id, budget_s):
@@ -232,7 +240,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default=WORKLOAD)
-    ap.add_argument("--ws", type=float, default=None)
+    ap.add_argument("--ws", default=None, help="target sliced width, or 'auto' (largest W_s whose plan fits HBM)")
     ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "fp32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -449,7 +457,8 @@ def main():
                            "d_sliced": str(ss.d), "sliced_labels": len(ss.labels),
                            "flops_per_slice": flops_slice, "slices_per_rank": K,
                            "l2": "per-slice working set > L2 (no flush needed)",
-                           "tree_source": meta["tree_source"], "precision": args.precision},
+                           "tree_source": meta["tree_source"], "precision": args.precision,
+                           "ws_auto": meta.get("ws_auto")},
                 "slices_per_s": slices_per_s,
                 "roofline": roofline, "cpu_baseline": cpu, "parity": parity,
                 "e2e": e2e, "clocks": clocks,

@@ -243,3 +243,32 @@ def iter_slice_assignments(tn, slice_set, start=0, stop=None):
     stop = d if stop is None else min(stop, d)
     for s in range(start, stop):
         yield dict(zip(labels, slice_digits(dims, s)))
+
+
+def auto_slice(tree, tn, device_bytes, ws_max=None, ws_min=None, fill=0.9, restarts=2, seed=0,
+               precision="3xtf32"):
+    """HBM-aware slicing: the largest target W_s whose
+    compiled plan -- the library's own arena plan (intermediates, GEMM operand
+    planes, split-K partials), persistent hoisted tensors and leaves -- fits in
+    ``fill * device_bytes``.  Larger W_s means fewer, larger slices and a lower
+    total cost C_s.  Returns (SliceSet, plan_bytes)."""
+    from .executor import SlicedPlan
+    from .tree import metrics
+    m = metrics(tree, tn)
+    hi = int(math.floor(m.width if ws_max is None else min(ws_max, m.width)))
+    lo = int(ws_min) if ws_min is not None else 1
+    for ws in range(hi, lo - 1, -1):
+        try:
+            ss = greedy_slice(tree, tn, ws, restarts=restarts, seed=seed) if ws < m.width else \
+                SliceSet.from_labels(tree, tn, ())
+        except ValueError:
+            break
+        plan = SlicedPlan(tn, tree, ss, precision=precision)
+        try:
+            st = plan.stats()
+            need = st["work_arena_bytes"] + st["persistent_bytes"] + st["leaf_bytes"]
+        finally:
+            plan.close()
+        if st["peak_elements"] < (1 << 40) and need <= fill * device_bytes:
+            return ss, need
+    raise ValueError("no slice width fits the device memory")

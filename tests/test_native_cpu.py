@@ -113,3 +113,15 @@ def test_accepts_reference_objects_when_available():
     assert plan.ops_per_slice * plan.d == sliced_metrics(rt, rtn, list(rtn.index_table)[:2])[1]
     assert plan.ops_per_slice * 1 <= rtree.metrics(rt, rtn).cost * 4
     plan.close()
+
+
+def test_auto_slice_fits_budget():
+    from paper_2002_01935_b200.slicing import auto_slice
+    from paper_2002_01935_b200.harness.paths import best_greedy_tree
+    tn = gen.grid_circuit(5, 5, 16, seed=2)
+    tree = best_greedy_tree(tn, trials=2)
+    big, need_big = auto_slice(tree, tn, 1 << 40)
+    assert big.labels == () or big.Ws == metrics(tree, tn).width
+    small, need_small = auto_slice(tree, tn, 4 << 20)
+    assert need_small <= 0.9 * (4 << 20) and small.Ws <= big.Ws
+    assert small.Cs >= big.Cs
