@@ -241,7 +241,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default=WORKLOAD)
     ap.add_argument("--ws", default=None, help="target sliced width, or 'auto' (largest W_s whose plan fits HBM)")
-    ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "fp32"])
+    ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "tf32-bf16x", "fp32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=90.0)
@@ -449,8 +449,9 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": K,
                 "warmup": W, "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "c64 (3xTF32 tcgen05 + FP32 SIMT)"
-                if args.precision == "3xtf32" else "c64 (FP32 SIMT)",
+                "vs_baseline": None, "dtype": {"3xtf32": "c64 (3xTF32 tcgen05 + FP32 SIMT)",
+                                               "tf32-bf16x": "c64 (TF32 hi*hi + BF16 cross terms, tcgen05)",
+                                               "fp32": "c64 (FP32 SIMT)"}[args.precision],
                 "data": "synthetic (seeded GRCS-style circuit, reference-driver tree)",
                 "config": {"workload": args.config, "desc": meta["desc"], "W": meta["W"],
                            "log10_C": meta["log10_C"], "W_s": ss.Ws, "log10_Cs": ss.log10_Cs,

@@ -43,9 +43,12 @@ typedef enum {
 
 typedef enum {
   TNX_PREC_FP32 = 0,     /* every contraction on FP32 SIMT kernels */
-  TNX_PREC_3XTF32 = 1    /* GEMM-shaped contractions on tcgen05 tensor cores,
+  TNX_PREC_3XTF32 = 1,   /* GEMM-shaped contractions on tcgen05 tensor cores,
                             split-TF32 (hi*hi + hi*lo + lo*hi), 4M complex,
                             FP32 accumulation in TMEM; the rest FP32 SIMT */
+  TNX_PREC_TF32_BF16X = 2 /* as 3XTF32 but the two small cross terms hi*lo +
+                            lo*hi run as BF16 MMAs (2x tensor rate, ~2^-20
+                            relative per product) */
 } tnx_precision;
 
 /* Leaf data element type / location for tnx_bind_leaves. */

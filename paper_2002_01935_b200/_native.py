@@ -13,7 +13,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libtnx.so")
 
 TNX_OK, TNX_ERR_INVALID, TNX_ERR_DATA, TNX_ERR_CUDA, TNX_ERR_OOM, TNX_ERR_NUMERIC, TNX_ERR_STATE = range(7)
-PREC_FP32, PREC_3XTF32 = 0, 1
+PREC_FP32, PREC_3XTF32, PREC_TF32_BF16X = 0, 1, 2
 DTYPE_C128, DTYPE_C64 = 0, 1
 LOC_HOST, LOC_DEVICE = 0, 1
 FLAG_NO_GRAPH, FLAG_NO_HOIST, FLAG_NO_TILED_PACK, FLAG_NO_DIRECT, FLAG_STRIP_EXPONENT = 1, 2, 4, 8, 16

@@ -112,6 +112,17 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t 
       : "memory");
 }
 
+// kind::f16 with BF16 operands (cross terms of the mixed TF32/BF16 mode)
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 __device__ __forceinline__ void umma_commit(uint32_t mbar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar)
@@ -152,6 +163,9 @@ struct GemmArgs {
   int64_t rows_a, rows_b;  // batch * M, batch * N (rows per plane)
   int32_t direct;        // 1: store as the parent's split-TF32 planes
   int32_t dvec;          // direct stores in float4 runs
+  int32_t mix;           // 1: TF32 hi*hi + BF16 cross terms (planes re_hi, re_x, im_hi, im_x)
+  int32_t dmix;          // direct planes in the mixed format ...
+  int32_t dside;         // ... for the parent's A (0) or B (1) operand
   float* dplanes;
   int64_t dplane_stride;
   IdxMap fmap, gmap;
@@ -192,6 +206,16 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& g, float2* out, i
 #pragma unroll
     for (int j = 0; j < 64; j += 4) {
       const int64_t off = f + gtab[hcol + j];
+      if (g.dmix) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          d[off + t] = tf32_hi(mre[j + t]);
+          d[off + 2 * ps + t] = tf32_hi(mim[j + t]);
+          store_mix_x(d + ps, off + t, mre[j + t], g.dside);
+          store_mix_x(d + 3 * ps, off + t, mim[j + t], g.dside);
+        }
+        continue;
+      }
       float rh[4], rl[4], ih[4], il[4];
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
@@ -219,9 +243,14 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& g, float2* out, i
       const float rh = __uint_as_float(__float_as_uint(re) & 0xffffe000u);
       const float ih = __uint_as_float(__float_as_uint(im) & 0xffffe000u);
       d[off] = rh;
-      d[off + ps] = re - rh;
       d[off + 2 * ps] = ih;
-      d[off + 3 * ps] = im - ih;
+      if (g.dmix) {
+        store_mix_x(d + ps, off, re, g.dside);
+        store_mix_x(d + 3 * ps, off, im, g.dside);
+      } else {
+        d[off + ps] = re - rh;
+        d[off + 3 * ps] = im - ih;
+      }
     }
     return;
   }
@@ -310,6 +339,15 @@ __device__ __forceinline__ void umma_tf32_2sm(uint32_t tmem_d, uint64_t a, uint6
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+__device__ __forceinline__ void umma_bf16_2sm(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void umma_commit_2sm(uint32_t mbar) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(mbar),
@@ -321,10 +359,11 @@ __device__ __forceinline__ void mbar_arrive_leader(uint32_t local_addr) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(0));
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
-// idesc: D=f32, A=B=tf32, K-major, N=128, M=128 (1 CTA) or 256 (pair)
+// idesc: D=f32, A=B=tf32 (fmt 2) or bf16 (fmt 1), K-major, N=128, M=128 (1 CTA)
+// or 256 (pair)
 template <bool TWO_SM>
-__host__ __device__ constexpr uint32_t idesc_mma(bool neg_a) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((neg_a ? 1u : 0u) << 13) |
+__host__ __device__ constexpr uint32_t idesc_mma(bool neg_a, uint32_t fmt = 2u) {
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | ((neg_a ? 1u : 0u) << 13) |
          ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((TWO_SM ? 256 : BM) >> 4) << 24);
 }
 
@@ -438,6 +477,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // ---------------- MMA issuer ----------------
       constexpr uint32_t ID_POS = idesc_mma<TWO_SM>(false);
       constexpr uint32_t ID_NEG = idesc_mma<TWO_SM>(true);
+      constexpr uint32_t ID_BP = idesc_mma<TWO_SM>(false, 1u);
+      constexpr uint32_t ID_BN = idesc_mma<TWO_SM>(true, 1u);
       int stage = 0;
       uint32_t phase = 0;
       uint32_t R = 0;  // global accumulator-round counter
@@ -472,6 +513,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const uint64_t bi_h = umma_desc_sw64(bb + 2 * C::B_BYTES);
               const uint64_t bi_l = umma_desc_sw64(bb + 3 * C::B_BYTES);
               const uint32_t acc0 = (kb > kb0 || ks > 0) ? 1u : 0u;
+              if (g.mix) {
+                // planes: 0 re_hi (tf32), 1 re_x (bf16 [hi|lo] / [lo|hi]), 2 im_hi, 3 im_x
+                if constexpr (TWO_SM) {
+                  umma_bf16_2sm(d_re, ar_l, br_l, ID_BP, acc0);
+                  umma_bf16_2sm(d_re, ai_l, bi_l, ID_BN, 1u);
+                  umma_tf32_2sm(d_re, ar_h, br_h, ID_POS, 1u);
+                  umma_tf32_2sm(d_re, ai_h, bi_h, ID_NEG, 1u);
+                  umma_bf16_2sm(d_im, ar_l, bi_l, ID_BP, acc0);
+                  umma_bf16_2sm(d_im, ai_l, br_l, ID_BP, 1u);
+                  umma_tf32_2sm(d_im, ar_h, bi_h, ID_POS, 1u);
+                  umma_tf32_2sm(d_im, ai_h, br_h, ID_POS, 1u);
+                } else {
+                  umma_bf16(d_re, ar_l, br_l, ID_BP, acc0);
+                  umma_bf16(d_re, ai_l, bi_l, ID_BN, 1u);
+                  umma_tf32(d_re, ar_h, br_h, ID_POS, 1u);
+                  umma_tf32(d_re, ai_h, bi_h, ID_NEG, 1u);
+                  umma_bf16(d_im, ar_l, bi_l, ID_BP, acc0);
+                  umma_bf16(d_im, ai_l, br_l, ID_BP, 1u);
+                  umma_tf32(d_im, ar_h, bi_h, ID_POS, 1u);
+                  umma_tf32(d_im, ai_h, br_h, ID_POS, 1u);
+                }
+                continue;
+              }
               if constexpr (TWO_SM) {
                 umma_tf32_2sm(d_re, ar_h, br_l, ID_POS, acc0);
                 umma_tf32_2sm(d_re, ar_l, br_h, ID_POS, 1u);
@@ -740,6 +804,9 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
   a.promote = g.promote > 0 ? g.promote : gemm_default_promote();
   a.direct = g.direct;
   a.dvec = g.dvec;
+  a.mix = g.mix;
+  a.dmix = g.dmix;
+  a.dside = g.dside;
   a.dplanes = g.dplanes;
   a.dplane_stride = g.dplane_stride;
   a.fmap = g.fmap;

@@ -326,9 +326,14 @@ __global__ void __launch_bounds__(256) pack_kernel(const PackParams p) {
     const float re_hi = __uint_as_float(__float_as_uint(re) & 0xffffe000u);
     const float im_hi = __uint_as_float(__float_as_uint(im) & 0xffffe000u);
     p.dst[e] = re_hi;
-    p.dst[e + p.plane_stride] = re - re_hi;
     p.dst[e + 2 * p.plane_stride] = im_hi;
-    p.dst[e + 3 * p.plane_stride] = im - im_hi;
+    if (p.mix) {
+      store_mix_x(p.dst + p.plane_stride, e, re, p.mix == 2);
+      store_mix_x(p.dst + 3 * p.plane_stride, e, im, p.mix == 2);
+    } else {
+      p.dst[e + p.plane_stride] = re - re_hi;
+      p.dst[e + 3 * p.plane_stride] = im - im_hi;
+    }
   }
 }
 
@@ -438,9 +443,16 @@ __global__ void __launch_bounds__(256) perm_vec_kernel(const PermParams p) {
         const float br = __uint_as_float(__float_as_uint(b.x) & 0xffffe000u);
         const float bi = __uint_as_float(__float_as_uint(b.y) & 0xffffe000u);
         *reinterpret_cast<float2*>(d + off) = make_float2(ar, br);
-        *reinterpret_cast<float2*>(d + off + p.plane_stride) = make_float2(a.x - ar, b.x - br);
         *reinterpret_cast<float2*>(d + off + 2 * p.plane_stride) = make_float2(ai, bi);
-        *reinterpret_cast<float2*>(d + off + 3 * p.plane_stride) = make_float2(a.y - ai, b.y - bi);
+        if (p.mode >= 3) {
+          store_mix_x(d + p.plane_stride, off, a.x, p.mode == 4);
+          store_mix_x(d + p.plane_stride, off + 1, b.x, p.mode == 4);
+          store_mix_x(d + 3 * p.plane_stride, off, a.y, p.mode == 4);
+          store_mix_x(d + 3 * p.plane_stride, off + 1, b.y, p.mode == 4);
+        } else {
+          *reinterpret_cast<float2*>(d + off + p.plane_stride) = make_float2(a.x - ar, b.x - br);
+          *reinterpret_cast<float2*>(d + off + 3 * p.plane_stride) = make_float2(a.y - ai, b.y - bi);
+        }
       }
     }
     __syncthreads();

@@ -541,7 +541,7 @@ int compile(Plan& P, const tnx_plan_desc* D) {
     TensorLoc& z = P.T[v.ssa];
     // tensor cores for GEMM-shaped vertices; small K (padded to 16) still
     // goes there when the output is large (SIMT would be output-bound)
-    const bool gemm = P.precision == TNX_PREC_3XTF32 && v.dxl.empty() && v.dyl.empty() &&
+    const bool gemm = P.precision != TNX_PREC_FP32 && v.dxl.empty() && v.dyl.empty() &&
                       v.M >= 128 && v.N >= 128 &&
                       (v.K >= 16 ? (double)v.macs >= P.gemm_min_macs : v.M * v.N >= (int64_t(1) << 20));
     if (gemm) {
@@ -610,7 +610,7 @@ int compile(Plan& P, const tnx_plan_desc* D) {
   //   * that child side becomes the child's row (A) side, and the child's rows
   //     and columns follow the parent's plane order, so the 32 lanes of an
   //     epilogue warp store consecutive floats (whole 128 B lines).
-  if (P.precision == TNX_PREC_3XTF32 && !(P.flags & TNX_FLAG_NO_DIRECT) &&
+  if (P.precision != TNX_PREC_FP32 && !(P.flags & TNX_FLAG_NO_DIRECT) &&
       !(P.flags & TNX_FLAG_STRIP_EXPONENT)) {
     auto in_list = [](const std::vector<int>& v, int l) {
       return std::find(v.begin(), v.end(), l) != v.end();
@@ -974,7 +974,8 @@ int lower(Plan& P) {
             PermParams pp;
             int64_t toff = 0;
             const size_t mark = P.ptabs.size();
-            if (build_perm(P, src, dst, 1, pp, toff, err)) {
+            const bool mixp = P.precision == TNX_PREC_TF32_BF16X;
+            if (build_perm(P, src, dst, mixp ? (side == 0 ? 3 : 4) : 1, pp, toff, err)) {
               pp.src = P.ptr(src);
               pp.dst = planes;
               pp.plane_stride = nrows * v.kp;
@@ -998,6 +999,7 @@ int lower(Plan& P) {
             pk.kp = v.kp;
             pk.plane_stride = nrows * v.kp;
             pk.nplanes = 4;
+            pk.mix = P.precision == TNX_PREC_TF32_BF16X ? (side == 0 ? 1 : 2) : 0;
             P.packs.push_back(pk);
             out.push_back({L_PACK, (int)P.packs.size() - 1, v.ssa});
           }
@@ -1006,6 +1008,7 @@ int lower(Plan& P) {
         float2* part = v.splits > 1 ? reinterpret_cast<float2*>(P.block_ptr(phase, v.blk_part)) : nullptr;
         if (gemm_prepare(&g, apl, bpl, P.ptr(z), v.B, ra, rb, v.kp, v.splits, part, ebuf, sizeof(ebuf)))
           return fail(TNX_ERR_CUDA, std::string("vertex ") + std::to_string(v.ssa) + ": " + ebuf);
+        g.mix = P.precision == TNX_PREC_TF32_BF16X ? 1 : 0;
         if (v.direct_parent >= 0) {
           const Vertex& pv = P.V[v.direct_parent - P.n];
           std::vector<int> pdst;
@@ -1021,6 +1024,8 @@ int lower(Plan& P) {
             return fail(TNX_ERR_INVALID, "vertex " + std::to_string(v.ssa) + ": " + err);
           const int64_t prows = pv.B * (v.direct_side == 0 ? (pv.swap ? pv.N : pv.M) : (pv.swap ? pv.M : pv.N));
           g.direct = 1;
+          g.dmix = g.mix;
+          g.dside = v.direct_side;
           g.dplanes = reinterpret_cast<float*>(
               P.block_ptr(phase, v.direct_side == 0 ? pv.blk_apl : pv.blk_bpl));
           g.dplane_stride = prows * pv.kp;
@@ -1196,7 +1201,7 @@ int tnx_bind_leaves(void* plan, const void* const* leaf_data, int32_t dtype, int
   TNX_CUDA(cudaSetDevice(P.device));
   if (!P.bound) {
     char ebuf[256];
-    if (P.precision == TNX_PREC_3XTF32 && gemm_init_attributes(ebuf, sizeof(ebuf)))
+    if (P.precision != TNX_PREC_FP32 && gemm_init_attributes(ebuf, sizeof(ebuf)))
       return fail(TNX_ERR_CUDA, ebuf);
     size_t free_b = 0, total_b = 0;
     TNX_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -1568,6 +1573,7 @@ int tnx_gemm_c64(const void* A, const void* B, void* C, int64_t batch, int64_t M
   pa.kp = kp;
   pa.plane_stride = pa.rows * kp;
   pa.nplanes = 4;
+  pa.mix = precision == TNX_PREC_TF32_BF16X ? 1 : 0;
   simple(pb.row, batch * N, K);
   simple(pb.col, K, 1);
   pb.src = static_cast<const float2*>(B);
@@ -1577,16 +1583,17 @@ int tnx_gemm_c64(const void* A, const void* B, void* C, int64_t batch, int64_t M
   pb.kp = kp;
   pb.plane_stride = pb.rows * kp;
   pb.nplanes = 4;
+  pb.mix = precision == TNX_PREC_TF32_BF16X ? 2 : 0;
   cudaError_t e = launch_pack(pa, st);
   if (e == cudaSuccess) e = launch_pack(pb, st);
   if (e != cudaSuccess) return fail(TNX_ERR_CUDA, cudaGetErrorString(e));
-  (void)precision;
   GemmPlan g;
   int splits = ((batch * M * N) % 2 == 0) ? gemm_choose_splits(batch, M, N, kp) : 1;
   float2* part = nullptr;
   if (splits > 1) TNX_CUDA(cudaMalloc(&part, 8 * (size_t)splits * batch * M * N));
   if (gemm_prepare(&g, apl, bpl, static_cast<float2*>(C), batch, M, N, kp, splits, part, ebuf, sizeof(ebuf)))
     return fail(TNX_ERR_CUDA, ebuf);
+  g.mix = precision == TNX_PREC_TF32_BF16X ? 1 : 0;
   e = launch_gemm(g, st);
   if (e != cudaSuccess) return fail(TNX_ERR_CUDA, cudaGetErrorString(e));
   TNX_CUDA(cudaStreamSynchronize(st));

@@ -4,6 +4,9 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#ifdef __CUDACC__
+#include <cuda_bf16.h>
+#endif
 
 namespace tnx {
 
@@ -52,8 +55,8 @@ struct PackParams {
   int64_t K;
   int64_t kp;
   int64_t plane_stride;   // rows * kp
-  int32_t nplanes;        // 4 or 6
-  int32_t pad;
+  int32_t nplanes;        // 4
+  int32_t mix;            // 0 split-TF32 planes, 1 mixed A-side, 2 mixed B-side
 };
 
 // Shared-memory tiled permutation (K2).  The tile spans the innermost source
@@ -70,7 +73,8 @@ struct PermParams {
   int64_t plane_stride;   // mode 1: elements per plane
   int32_t ts;
   int32_t group;
-  int32_t mode;           // 0: complex64 copy, 1: 4 split-TF32 planes
+  int32_t mode;           // 0: complex64 copy, 1: 4 split-TF32 planes,
+                          // 3 / 4: mixed TF32/BF16 planes for an A / B operand
   int32_t vec;            // 1: element pairs contiguous + aligned on both sides
   int32_t ts_log2;        // log2(ts) if ts is a power of two, else -1
   int32_t pad;
@@ -124,6 +128,28 @@ struct AccumParams {
   long long* acc_exp;
 };
 
+#ifdef __CUDACC__
+// Mixed TF32/BF16 operand planes: plane words are laid out like the split-TF32
+// planes ([kp/16][rows][16] 4-byte words); the bf16 "x" plane stores, per
+// 16-wide k-block row, 32 bf16 = [hi(16) | lo(16)] for the A operand and
+// [lo(16) | hi(16)] for B, so one bf16 MMA chunk pairs A.hi with B.lo and the
+// next A.lo with B.hi (the two cross terms of the split product).
+__device__ __forceinline__ float tf32_hi(float v) {
+  return __uint_as_float(__float_as_uint(v) & 0xffffe000u);
+}
+__device__ __forceinline__ void store_mix_x(float* plane_x, int64_t e, float v, int side_b) {
+  const float hi = tf32_hi(v);
+  const float lo = v - hi;
+  unsigned short* hw = reinterpret_cast<unsigned short*>(plane_x);
+  const int64_t ki = e & 15;
+  const int64_t base = 2 * (e - ki);
+  const unsigned short hb = __bfloat16_as_ushort(__float2bfloat16_rn(hi));
+  const unsigned short lb = __bfloat16_as_ushort(__float2bfloat16_rn(lo));
+  hw[base + (side_b ? 16 : 0) + ki] = hb;
+  hw[base + (side_b ? 0 : 16) + ki] = lb;
+}
+#endif
+
 // launchers (return cudaError_t)
 cudaError_t launch_gather(const GatherJob* jobs, int njobs, const float2* leaf_pool,
                           const unsigned long long* slice_counter, cudaStream_t st);
@@ -157,6 +183,10 @@ struct GemmPlan {
   // planes (offset = fmap(row) + gmap(col)) instead of complex64 `out`
   int32_t direct;
   int32_t dvec;           // direct stores as float4 runs of 4 columns
+  int32_t mix;            // mixed TF32/BF16 mode (operand planes and MMA sequence)
+  int32_t dmix;           // direct planes in the mixed format for parent side dside
+  int32_t dside;
+  int32_t pad2;
   float* dplanes;
   int64_t dplane_stride;
   IdxMap fmap;            // output row (batch*M + m) -> plane offset (st0)

@@ -31,7 +31,7 @@ from .network import DataError, TensorNetwork, TensorNode
 __all__ = ["SlicedPlan", "contract", "contract_sliced", "amplitude", "AmplitudeEngine",
            "PRECISIONS"]
 
-PRECISIONS = {"fp32": nat.PREC_FP32, "3xtf32": nat.PREC_3XTF32}
+PRECISIONS = {"fp32": nat.PREC_FP32, "3xtf32": nat.PREC_3XTF32, "tf32-bf16x": nat.PREC_TF32_BF16X}
 
 
 def _as_labels(slice_set):

@@ -17,7 +17,7 @@ from paper_2002_01935_b200.tree import ContractionTree
 for (lm, ln, lk) in [(13, 13, 12), (12, 12, 14), (11, 11, 16)]:
     tn = net(lm, ln, lk, 0)
     tree = ContractionTree((0, 1), [(0, 1)])
-    plan = SlicedPlan(tn, tree, ()).bind()
+    plan = SlicedPlan(tn, tree, (), precision=os.environ.get('PREC', '3xtf32')).bind()
     prof = plan.profile_slice(0)
     g = [t for k, v, t in prof if k == "gemm"]
     plan.run(); val = plan.result()
@@ -25,6 +25,6 @@ for (lm, ln, lk) in [(13, 13, 12), (12, 12, 14), (11, 11, 16)]:
     ref = (x @ y.T).reshape(val.shape)
     err = np.linalg.norm(val - ref) / np.linalg.norm(ref)
     fl = 8 * 2**(lm+ln+lk)
-    print(f"promote={os.environ.get('TNX_GEMM_PROMOTE','2')} M=2^{lm} N=2^{ln} K=2^{lk}: gemm {g[0]:.3f} ms "
+    print(f"prec={os.environ.get('PREC','3xtf32')} M=2^{lm} N=2^{ln} K=2^{lk}: gemm {g[0]:.3f} ms "
           f"{fl/g[0]/1e9:.1f} TF/s  rel_err {err:.2e}", flush=True)
     plan.close()
