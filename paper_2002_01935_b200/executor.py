@@ -32,6 +32,12 @@ __all__ = ["SlicedPlan", "contract", "contract_sliced", "amplitude", "AmplitudeE
            "PRECISIONS"]
 
 PRECISIONS = {"fp32": nat.PREC_FP32, "3xtf32": nat.PREC_3XTF32, "tf32-bf16x": nat.PREC_TF32_BF16X}
+DEFAULT_PRECISION = "3xtf32"
+
+
+def _precision(p):
+    import os
+    return p if p is not None else os.environ.get("TNX_PRECISION", DEFAULT_PRECISION)
 
 
 def _as_labels(slice_set):
@@ -56,7 +62,7 @@ class SlicedPlan:
     contracts a slice range into the device accumulator.
     """
 
-    def __init__(self, tn, tree, slice_set=(), device=0, precision="3xtf32", graph=True,
+    def __init__(self, tn, tree, slice_set=(), device=0, precision=None, graph=True,
                  hoist=True, gemm_min_macs=0.0, tiled_pack=True, direct_planes=True,
                  strip_exponent=False):
         lib = nat.load()
@@ -90,6 +96,7 @@ class SlicedPlan:
             ranks=_i32(ranks), leaf_labels=_i32(leaf_labels), pairs=_i32(pairs),
             out=_i32([lid[l] for l in tn.output]), sl=_i32([lid[l] for l in self.sliced]))
         k = self._keep
+        precision = _precision(precision)
         flags = ((0 if graph else nat.FLAG_NO_GRAPH) | (0 if hoist else nat.FLAG_NO_HOIST)
                  | (0 if tiled_pack else nat.FLAG_NO_TILED_PACK)
                  | (0 if direct_planes else nat.FLAG_NO_DIRECT)
@@ -333,7 +340,7 @@ def _slice_range(d, slice_ids):
 
 
 def contract_sliced(tn, tree, slice_set=(), options=None, *, slice_ids=None, devices=(0,),
-                    precision="3xtf32", graph=True, hoist=True):
+                    precision=None, graph=True, hoist=True):
     """Sum over slice assignments of the per-slice contraction.
 
     Returns (value-or-open-tensor, exponent10, op_count) with op_count the
@@ -421,7 +428,7 @@ class AmplitudeEngine:
     """One compiled plan reused across bitstrings (only leaf data changes,
     PAPER.md:530; SPEC.md:533-537)."""
 
-    def __init__(self, circuit_tn, tree, slice_set=(), device=0, precision="3xtf32"):
+    def __init__(self, circuit_tn, tree, slice_set=(), device=0, precision=None):
         self.tn = circuit_tn
         self.tree = tree
         base = _project(circuit_tn, "0" * len(circuit_tn.output))

@@ -13,7 +13,7 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg4_7x7_d40"
 sid = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 ws = float(sys.argv[3]) if len(sys.argv) > 3 else None
 tn, tree, ss, meta = load_workload(cfg, ws=ws)
-plan = SlicedPlan(tn, tree, ss, direct_planes=False).bind()
+plan = SlicedPlan(tn, tree, ss, direct_planes=False).bind()  # precision from TNX_PRECISION
 info = {v["ssa"]: v for v in plan.vertex_info()}
 rec = {}
 t = time.time()
