@@ -786,7 +786,7 @@ static int gemm_default_promote() {
   static int v = 0;
   if (!v) {
     const char* e = getenv("TNX_GEMM_PROMOTE");
-    v = e ? atoi(e) : 4;
+    v = e ? atoi(e) : 2;
     if (v < 1) v = 1;
   }
   return v;
