@@ -196,7 +196,7 @@ def test_direct_planes_fusion_matches_materialised():
             fused = [v["ssa"] for v in plan.vertex_info() if v["kind"] == "gemm_tc"]
             assert plan.stats()["num_gemm"] >= 2
         plan.close()
-    assert rel_err(vals[0], vals[1]) <= 2e-6
+    assert rel_err(vals[0], vals[1]) <= 5e-6
     ref, _, _ = oracle.contract_sliced(tn, tree, ss.labels, slice_ids=range(0, 8))
     assert rel_err(vals[0], ref) <= TOL
 
