@@ -8,7 +8,7 @@ from paper_2002_01935_b200.harness.workloads import load_workload
 for name, ws in (("cfg4p_7x7_d16", 16), ("cfg4p_7x7_d20", 24), ("cfg4p_7x7_d20", 21)):
     tn, tree, ss, _ = load_workload(name, ws=ws)
     ref, _, _ = oracle.contract(tn, tree)
-    for prec in ("3xtf32", "tf32-bf16x", "fp32"):
+    for prec in os.environ.get("PRECS", "3xtf32,tf32-bf16x,fp32").split(","):
         plan = SlicedPlan(tn, tree, ss, precision=prec).bind()
         plan.run()
         got = complex(plan.result())
