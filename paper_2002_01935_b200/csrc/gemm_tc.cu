@@ -146,6 +146,19 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
       : "r"(taddr));
 }
 
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -600,15 +613,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc_fence_after();
         const uint32_t t0 = lane_base + set * 256;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          uint32_t re[16], im[16];
-          tmem_ld16(t0 + j * 16, re);
-          tmem_ld16(t0 + BN + j * 16, im);
+        for (int j = 0; j < 2; ++j) {
+          uint32_t re[32], im[32];
+          tmem_ld32(t0 + j * 32, re);
+          tmem_ld32(t0 + BN + j * 32, im);
           tmem_wait_ld();
 #pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            mre[j * 16 + t] += __uint_as_float(re[t]);
-            mim[j * 16 + t] += __uint_as_float(im[t]);
+          for (int t = 0; t < 32; ++t) {
+            mre[j * 32 + t] += __uint_as_float(re[t]);
+            mim[j * 32 + t] += __uint_as_float(im[t]);
           }
         }
         tc_fence_before();
@@ -786,7 +799,7 @@ static int gemm_default_promote() {
   static int v = 0;
   if (!v) {
     const char* e = getenv("TNX_GEMM_PROMOTE");
-    v = e ? atoi(e) : 2;
+    v = e ? atoi(e) : 3;
     if (v < 1) v = 1;
   }
   return v;
