@@ -248,6 +248,8 @@ def main():
     ap.add_argument("--profile-out", default=None)
     ap.add_argument("--no-tf32-probe", action="store_true")
     ap.add_argument("--no-direct", action="store_true", help="disable GEMM->GEMM operand-plane fusion")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="initialise torch.distributed even at world size 1 (exercises the NCCL path)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -265,7 +267,13 @@ def main():
     backend = os.environ.get("TNX_BENCH_BACKEND", "nccl")
     local = local % torch.cuda.device_count() if backend != "nccl" else local
     torch.cuda.set_device(local)
-    if world > 1:
+    use_dist = world > 1 or args.force_dist
+    if use_dist:
+        if "MASTER_ADDR" not in os.environ:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -294,7 +302,7 @@ def main():
     red_dev = "cuda" if backend == "nccl" else "cpu"
 
     def barrier():
-        if world > 1:
+        if use_dist:
             if backend == "nccl":
                 dist.barrier(device_ids=[local])
             else:
@@ -320,7 +328,7 @@ def main():
     clocks = clk.stop()
     ms = e0.elapsed_time(e1)
     t_max = torch.tensor([ms], dtype=torch.float64, device=red_dev)
-    if world > 1:
+    if use_dist:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     ms_max = float(t_max.item())
 
@@ -419,7 +427,7 @@ def main():
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
         t_e = torch.tensor([e2e_s], dtype=torch.float64, device=red_dev)
-        if world > 1:
+        if use_dist:
             dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
         e2e_s = float(t_e.item())
         e2e = {"value": total_slices * flops_slice / e2e_s / 1e12, "unit": "TFLOP/s",
@@ -466,11 +474,11 @@ def main():
                 "gpu_launches": K * st["launches_per_slice"],
                 "plan": {k: st[k] for k in ("num_gemm", "num_simt", "num_hoisted", "launches_per_slice",
                                             "work_arena_bytes")},
-                "allreduce_ms": allreduce_ms, "setup_s": setup_s, "backend": backend if world > 1 else None,
+                "allreduce_ms": allreduce_ms, "setup_s": setup_s, "backend": backend if use_dist else None,
                 "prefix_sum": [complex(np.asarray(total).ravel()[0]).real, complex(np.asarray(total).ravel()[0]).imag]}
         print(json.dumps(line, default=str))
     plan.close()
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
     return 0
 

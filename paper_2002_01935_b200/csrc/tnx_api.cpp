@@ -197,7 +197,7 @@ struct Plan {
   std::vector<int> level;          // slice-phase dependency level per vertex index
   std::vector<GemmPlan> gemms;
   AccumParams accum{};
-  std::vector<float2> staging;
+  float2* staging = nullptr;       // pinned host staging for complex128 leaf uploads
 
   ~Plan() { release(); }
   void release() {
@@ -224,6 +224,8 @@ struct Plan {
     counter = nullptr;
     if (own) cudaStreamDestroy(own);
     own = nullptr;
+    if (staging) cudaFreeHost(staging);
+    staging = nullptr;
     bound = false;
   }
 
@@ -1298,14 +1300,18 @@ int tnx_bind_leaves(void* plan, const void* const* leaf_data, int32_t dtype, int
   for (int i = 0; i < P.n; ++i) max_leaf = std::max<int64_t>(max_leaf, P.prod(P.leaf_labels[i]));
   if (location == TNX_LOC_HOST) {
     if (dtype == TNX_DTYPE_C128) {
-      P.staging.assign(P.pool_elems, make_float2(0.f, 0.f));
+      if (!P.staging) {
+        TNX_CUDA(cudaMallocHost(&P.staging, P.pool_elems * 8));
+        std::memset(P.staging, 0, P.pool_elems * 8);
+      }
+      TNX_CUDA(cudaStreamSynchronize(st));  // previous upload finished reading the staging buffer
       for (int i = 0; i < P.n; ++i) {
         const double* src = static_cast<const double*>(leaf_data[i]);
         int64_t sz = P.prod(P.leaf_labels[i]);
         for (int64_t e = 0; e < sz; ++e)
           P.staging[P.pool_off[i] + e] = make_float2((float)src[2 * e], (float)src[2 * e + 1]);
       }
-      TNX_CUDA(cudaMemcpyAsync(P.pool, P.staging.data(), P.pool_elems * 8, cudaMemcpyHostToDevice, st));
+      TNX_CUDA(cudaMemcpyAsync(P.pool, P.staging, P.pool_elems * 8, cudaMemcpyHostToDevice, st));
     } else {
       for (int i = 0; i < P.n; ++i)
         TNX_CUDA(cudaMemcpyAsync(P.pool + P.pool_off[i], leaf_data[i], P.prod(P.leaf_labels[i]) * 8,

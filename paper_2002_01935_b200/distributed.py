@@ -38,13 +38,13 @@ def allreduce_complex(arr, group=None, device=None):
     t = torch.from_numpy(a.view(np.float64).copy())
     if device is not None:
         t = t.to(device)
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+    if dist.is_available() and dist.is_initialized():
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     out = t.cpu().numpy().view(np.complex128)
     return out.reshape(np.shape(arr)) if np.ndim(arr) else out[0]
 
 
-def contract_sliced_distributed(tn, tree, slice_set, s_begin=0, s_end=None, precision="3xtf32",
+def contract_sliced_distributed(tn, tree, slice_set, s_begin=0, s_end=None, precision=None,
                                 group=None):
     """Each rank contracts its block on its local GPU; returns the global sum
     on every rank (requires an initialised process group)."""
