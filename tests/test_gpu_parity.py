@@ -346,3 +346,43 @@ def test_gemm_path_odd_dims(dims):
     # sliced on a K label and a batch label
     val, _, _ = contract_sliced(tn, tree, ["k1", "b"])
     assert rel_err(val, ref) <= 2e-6
+
+
+def test_edge_cases_single_leaf_hyperedge_dim1():
+    from paper_2002_01935_b200.network import from_arrays
+    from paper_2002_01935_b200.tree import ContractionTree
+    rng = np.random.default_rng(11)
+    # single-node network, output subset, sliced dangling label
+    a = rng.standard_normal((2, 3, 4)) + 1j * rng.standard_normal((2, 3, 4))
+    tn = from_arrays("abc->ca", [a])
+    tree = ContractionTree((0,), [])
+    for S in ((), ("b",)):
+        ref, _, _ = oracle.contract_sliced(tn, tree, S)
+        got, _, ops = contract_sliced(tn, tree, S)
+        assert rel_err(got, ref) <= 1e-6 and ops == 0
+    # hyperedge label on three leaves, sliced; a dim-1 label; open output
+    x = rng.standard_normal((2, 1, 3)) + 0j
+    y = rng.standard_normal((2, 3, 2)) + 1j
+    z = rng.standard_normal((2, 2)) - 1j
+    tn = from_arrays("hqa,hab,hb->q", [x, y, z])
+    tree = ContractionTree((0, 1, 2), [(0, 1), (3, 2)])
+    for S in ((), ("h",), ("h", "a"), ("b",)):
+        ref, _, _ = oracle.contract_sliced(tn, tree, S)
+        got, _, _ = contract_sliced(tn, tree, S)
+        assert rel_err(got, ref) <= 1e-6, S
+
+
+def test_sliced_label_without_carrier_multiplies_by_dim():
+    """A sliced index carried by no tensor contributes a factor d (every slice
+    is identical) -- same as the oracle's slice loop."""
+    from paper_2002_01935_b200.network import TensorNetwork, TensorNode
+    from paper_2002_01935_b200.tree import ContractionTree
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((2, 2)) + 0j
+    y = rng.standard_normal((2, 2)) + 0j
+    tn = TensorNetwork([TensorNode(0, "ab", x), TensorNode(1, "ba", y)], {"a": 2, "b": 2, "z": 3}, ())
+    tree = ContractionTree((0, 1), [(0, 1)])
+    ref, _, _ = oracle.contract_sliced(tn, tree, ["z"])
+    got, _, _ = contract_sliced(tn, tree, ["z"])
+    assert abs(got - ref) <= 1e-6 * abs(ref)
+    assert abs(ref - 3 * np.trace(x @ y)) <= 1e-12 * abs(ref)
