@@ -60,19 +60,38 @@ __device__ __forceinline__ void cfma(float2& acc, float2 a, float2 b) {
 }
 
 // ------------------------------------------------------------------ gather
-__global__ void gather_kernel(const GatherJob* __restrict__ jobs, const float2* __restrict__ pool,
-                              const unsigned long long* __restrict__ counter) {
-  const GatherJob& j = jobs[blockIdx.x];
+// One launch for all slice-dependent leaves: each job owns a contiguous range of
+// blocks (prefix table `start`, sized on the host in proportion to the leaf
+// slice), so one large leaf is spread over the whole GPU while tiny circuit
+// leaves take one block each.  Kept dims are pre-merged into contiguous runs.
+__global__ void __launch_bounds__(256) gather_kernel(const GatherJob* __restrict__ jobs,
+                                                     const int32_t* __restrict__ start, int njobs,
+                                                     const float2* __restrict__ pool,
+                                                     const unsigned long long* __restrict__ counter) {
+  int lo = 0, hi = njobs - 1;
+  const int b = blockIdx.x;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (start[mid] <= b) lo = mid;
+    else hi = mid - 1;
+  }
+  const GatherJob& j = jobs[lo];
+  const int lb = b - start[lo];
+  const int nb = start[lo + 1] - start[lo];
   const unsigned long long s = *counter;
   int64_t base = j.src;
   for (int i = 0; i < j.n_sl; ++i) {
     unsigned long long digit = (s / j.radix[i]) % (unsigned long long)j.sdim[i];
     base += (int64_t)digit * j.sst[i];
   }
-  for (int64_t e = threadIdx.x; e < j.out_size; e += blockDim.x) {
-    int64_t off = base, idx = e;
-    for (int i = j.n_kept - 1; i >= 0; --i) {
-      int64_t q = idx / j.kdim[i];
+  const int nk = j.n_kept;
+  const int64_t inner = nk > 0 ? j.kdim[nk - 1] : 1;
+  const int64_t inner_st = nk > 0 ? j.kst[nk - 1] : 0;
+  for (int64_t e = (int64_t)lb * blockDim.x + threadIdx.x; e < j.out_size; e += (int64_t)nb * blockDim.x) {
+    int64_t idx = e / inner;
+    int64_t off = base + (e - idx * inner) * inner_st;
+    for (int i = nk - 2; i >= 0; --i) {
+      const int64_t q = idx / j.kdim[i];
       off += (idx - q * j.kdim[i]) * j.kst[i];
       idx = q;
     }
@@ -80,10 +99,10 @@ __global__ void gather_kernel(const GatherJob* __restrict__ jobs, const float2* 
   }
 }
 
-cudaError_t launch_gather(const GatherJob* jobs, int njobs, const float2* pool,
-                          const unsigned long long* counter, cudaStream_t st) {
+cudaError_t launch_gather(const GatherJob* jobs, const int32_t* start, int njobs, int total_blocks,
+                          const float2* pool, const unsigned long long* counter, cudaStream_t st) {
   if (njobs == 0) return cudaSuccess;
-  gather_kernel<<<njobs, 64, 0, st>>>(jobs, pool, counter);
+  gather_kernel<<<total_blocks, 256, 0, st>>>(jobs, start, njobs, pool, counter);
   return cudaGetLastError();
 }
 
@@ -396,10 +415,20 @@ __global__ void __launch_bounds__(256) perm_kernel(const PermParams p) {
 }
 
 // Vectorised variant: element pairs (t, t+1) are contiguous and 16 B / 8 B
-// aligned in source and destination, ts is a power of two.
-__global__ void __launch_bounds__(256) perm_vec_kernel(const PermParams p) {
+// aligned in source and destination, ts is a power of two.  Software-pipelined:
+// the global loads of chunk c+1 are issued into registers before chunk c is
+// stored, so every SM keeps loads in flight through the store phase.  The tile
+// is XOR-swizzled on float2 bits 1..3 (pairs stay adjacent and 16 B aligned, so
+// the store side reads float4) to spread the transposed writes over the banks.
+__device__ __forceinline__ int perm_swz(int i) {
+  return i ^ ((((i >> 4) ^ (i >> 7) ^ (i >> 10)) & 7) << 1);
+}
+
+constexpr int kPermMaxPairs = 4;  // (ts * group / 2) / 256 <= 2048 / 2 / 256 (vec needs ts <= 2048)
+
+__global__ void __launch_bounds__(256, 4) perm_vec_kernel(const PermParams p) {
   extern __shared__ __align__(16) unsigned char perm_smem[];
-  __shared__ int64_t base_s[64], base_d[64];
+  __shared__ int64_t base_s[2][64], base_d[2][64];
   const int ts = p.ts;
   const int lg = p.ts_log2;
   const int G = p.group;
@@ -412,50 +441,83 @@ __global__ void __launch_bounds__(256) perm_vec_kernel(const PermParams p) {
   const int half_mask = (ts >> 1) - 1;
   const int half_lg = lg - 1;
   float* d = static_cast<float*>(p.dst);
-  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+  auto count_of = [&](int64_t c) {
     const int64_t o0 = c * G;
-    const int gcount = (int)(p.n_outer - o0 < (int64_t)G ? p.n_outer - o0 : (int64_t)G);
-    if (threadIdx.x < gcount) {
+    return (int)(p.n_outer - o0 < (int64_t)G ? p.n_outer - o0 : (int64_t)G);
+  };
+  auto bases = [&](int64_t c, int buf) {
+    if (threadIdx.x < count_of(c)) {
       int64_t sb = 0, db = 0;
-      decode2(p.outer, o0 + threadIdx.x, sb, db);
-      base_s[threadIdx.x] = sb;
-      base_d[threadIdx.x] = db;
+      decode2(p.outer, c * G + threadIdx.x, sb, db);
+      base_s[buf][threadIdx.x] = sb;
+      base_d[buf][threadIdx.x] = db;
     }
-    __syncthreads();
-    const int npairs = gcount << half_lg;
-    for (int e = threadIdx.x; e < npairs; e += blockDim.x) {
-      const int j = e >> half_lg, t = (e & half_mask) << 1;
-      const float4 v = *reinterpret_cast<const float4*>(p.src + base_s[j] + t_src[t]);
-      tile[(j << lg) + t_idx[t]] = make_float2(v.x, v.y);
-      tile[(j << lg) + t_idx[t + 1]] = make_float2(v.z, v.w);
+  };
+  float4 r[kPermMaxPairs];
+  auto issue = [&](int buf, int npairs) {
+#pragma unroll
+    for (int i = 0; i < kPermMaxPairs; ++i) {
+      const int e = threadIdx.x + i * 256;
+      if (e < npairs) {
+        const int j = e >> half_lg, t = (e & half_mask) << 1;
+        r[i] = __ldg(reinterpret_cast<const float4*>(p.src + base_s[buf][j] + t_src[t]));
+      }
     }
+  };
+  int64_t c = blockIdx.x;
+  if (c >= nchunks) return;
+  int buf = 0;
+  bases(c, 0);
+  __syncthreads();
+  int npairs = count_of(c) << half_lg;
+  issue(0, npairs);
+  while (true) {
+#pragma unroll
+    for (int i = 0; i < kPermMaxPairs; ++i) {
+      const int e = threadIdx.x + i * 256;
+      if (e < npairs) {
+        const int j = e >> half_lg, t = (e & half_mask) << 1;
+        tile[perm_swz((j << lg) + t_idx[t])] = make_float2(r[i].x, r[i].y);
+        tile[perm_swz((j << lg) + t_idx[t + 1])] = make_float2(r[i].z, r[i].w);
+      }
+    }
+    const int64_t cn = c + gridDim.x;
+    const bool more = cn < nchunks;
+    if (more) bases(cn, buf ^ 1);
     __syncthreads();
-    for (int e = threadIdx.x; e < npairs; e += blockDim.x) {
+    const int np_cur = npairs;
+    if (more) {
+      npairs = count_of(cn) << half_lg;
+      issue(buf ^ 1, npairs);
+    }
+    for (int e = threadIdx.x; e < np_cur; e += blockDim.x) {
       const int j = e >> half_lg, t = (e & half_mask) << 1;
-      const float2 a = tile[(j << lg) + t];
-      const float2 b = tile[(j << lg) + t + 1];
-      const int64_t off = base_d[j] + t_dst[t];
+      const float4 v = *reinterpret_cast<const float4*>(tile + perm_swz((j << lg) + t));
+      const int64_t off = base_d[buf][j] + t_dst[t];
       if (p.mode == 0) {
-        *reinterpret_cast<float4*>(static_cast<float2*>(p.dst) + off) = make_float4(a.x, a.y, b.x, b.y);
+        __stcs(reinterpret_cast<float4*>(static_cast<float2*>(p.dst) + off), v);
       } else {
-        const float ar = __uint_as_float(__float_as_uint(a.x) & 0xffffe000u);
-        const float ai = __uint_as_float(__float_as_uint(a.y) & 0xffffe000u);
-        const float br = __uint_as_float(__float_as_uint(b.x) & 0xffffe000u);
-        const float bi = __uint_as_float(__float_as_uint(b.y) & 0xffffe000u);
+        const float ar = __uint_as_float(__float_as_uint(v.x) & 0xffffe000u);
+        const float ai = __uint_as_float(__float_as_uint(v.y) & 0xffffe000u);
+        const float br = __uint_as_float(__float_as_uint(v.z) & 0xffffe000u);
+        const float bi = __uint_as_float(__float_as_uint(v.w) & 0xffffe000u);
         *reinterpret_cast<float2*>(d + off) = make_float2(ar, br);
         *reinterpret_cast<float2*>(d + off + 2 * p.plane_stride) = make_float2(ai, bi);
         if (p.mode >= 3) {
-          store_mix_x(d + p.plane_stride, off, a.x, p.mode == 4);
-          store_mix_x(d + p.plane_stride, off + 1, b.x, p.mode == 4);
-          store_mix_x(d + 3 * p.plane_stride, off, a.y, p.mode == 4);
-          store_mix_x(d + 3 * p.plane_stride, off + 1, b.y, p.mode == 4);
+          store_mix_x(d + p.plane_stride, off, v.x, p.mode == 4);
+          store_mix_x(d + p.plane_stride, off + 1, v.z, p.mode == 4);
+          store_mix_x(d + 3 * p.plane_stride, off, v.y, p.mode == 4);
+          store_mix_x(d + 3 * p.plane_stride, off + 1, v.w, p.mode == 4);
         } else {
-          *reinterpret_cast<float2*>(d + off + p.plane_stride) = make_float2(a.x - ar, b.x - br);
-          *reinterpret_cast<float2*>(d + off + 3 * p.plane_stride) = make_float2(a.y - ai, b.y - bi);
+          *reinterpret_cast<float2*>(d + off + p.plane_stride) = make_float2(v.x - ar, v.z - br);
+          *reinterpret_cast<float2*>(d + off + 3 * p.plane_stride) = make_float2(v.y - ai, v.w - bi);
         }
       }
     }
+    if (!more) break;
     __syncthreads();
+    c = cn;
+    buf ^= 1;
   }
 }
 
@@ -464,8 +526,14 @@ cudaError_t launch_perm(const PermParams& p, cudaStream_t st) {
   const int64_t nchunks = (p.n_outer + p.group - 1) / p.group;
   int blocks = (int)std::min<int64_t>(nchunks, 148 * 8);
   if (blocks < 1) blocks = 1;
-  if (p.vec)
+  if (p.vec && p.ts * p.group <= 2048) {
+    static bool carveout = [] {
+      cudaFuncSetAttribute(perm_vec_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      return true;
+    }();
+    (void)carveout;
     perm_vec_kernel<<<blocks, 256, smem, st>>>(p);
+  }
   else
     perm_kernel<<<blocks, 256, smem, st>>>(p);
   return cudaGetLastError();

@@ -167,7 +167,9 @@ struct Plan {
   float2* partial = nullptr;
   Int2Off* d_tabs = nullptr;
   GatherJob* d_jobs = nullptr;
+  int32_t* d_gstart = nullptr;
   int njobs = 0;
+  int gather_blocks = 0;
   double2* acc = nullptr;
   double2* comp = nullptr;
   unsigned long long* counter = nullptr;
@@ -206,7 +208,7 @@ struct Plan {
     gexec = nullptr;
     graph = nullptr;
     void* ptrs[] = {pool,    work,   persist, partial, d_tabs,    d_jobs,   acc,    comp,
-                    counter, d_ptabs, d_bjobs, d_bstarts, d_absmax, d_exps, d_acc_exp};
+                    counter, d_ptabs, d_bjobs, d_bstarts, d_absmax, d_exps, d_acc_exp, d_gstart};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     pool = nullptr;
@@ -220,6 +222,7 @@ struct Plan {
     d_exps = nullptr;
     d_acc_exp = nullptr;
     d_jobs = nullptr;
+    d_gstart = nullptr;
     acc = comp = nullptr;
     counter = nullptr;
     if (own) cudaStreamDestroy(own);
@@ -774,13 +777,15 @@ bool build_perm(Plan& P, const TensorLoc& t, const std::vector<int>& dst, int mo
   std::memset(&pp, 0, sizeof(pp));
   if (t.size >= (int64_t(1) << 31)) return false;
   std::vector<char> in_tile(P.L, 0);
+  static const int64_t run_src = getenv("TNX_PERM_SRC") ? atoll(getenv("TNX_PERM_SRC")) : 32;
+  static const int64_t run_dst = getenv("TNX_PERM_DST") ? atoll(getenv("TNX_PERM_DST")) : 32;
   int64_t prod = 1;
-  for (int i = (int)t.labels.size() - 1; i >= 0 && prod < 32; --i) {
+  for (int i = (int)t.labels.size() - 1; i >= 0 && prod < run_src; --i) {
     prod *= P.dims[t.labels[i]];
     in_tile[t.labels[i]] = 1;
   }
   prod = 1;
-  for (int i = (int)dst.size() - 1; i >= 0 && prod < 32; --i) {
+  for (int i = (int)dst.size() - 1; i >= 0 && prod < run_dst; --i) {
     prod *= P.dims[dst[i]];
     in_tile[dst[i]] = 1;
   }
@@ -865,7 +870,7 @@ int run_launches(Plan& P, const std::vector<Launch>& ls, cudaStream_t st, int st
     cudaError_t e = cudaSuccess;
     switch (L.type) {
       case L_GATHER:
-        e = launch_gather(P.d_jobs, P.njobs, P.pool, P.counter, st);
+        e = launch_gather(P.d_jobs, P.d_gstart, P.njobs, P.gather_blocks, P.pool, P.counter, st);
         break;
       case L_SIMT:
         e = launch_simt(P.simt[L.idx], st);
@@ -1255,6 +1260,9 @@ int tnx_bind_leaves(void* plan, const void* const* leaf_data, int32_t dtype, int
           j.sdim[j.n_sl] = P.dims[l];
           j.sst[j.n_sl] = st[q];
           j.n_sl++;
+        } else if (j.n_kept > 0 && j.kst[j.n_kept - 1] == st[q] * P.dims[l]) {
+          j.kdim[j.n_kept - 1] *= P.dims[l];  // merge into the previous contiguous run
+          j.kst[j.n_kept - 1] = st[q];
         } else {
           j.kdim[j.n_kept] = P.dims[l];
           j.kst[j.n_kept] = st[q];
@@ -1265,8 +1273,16 @@ int tnx_bind_leaves(void* plan, const void* const* leaf_data, int32_t dtype, int
     }
     P.njobs = (int)jobs.size();
     if (P.njobs) {
+      std::vector<int32_t> gstart(1, 0);
+      for (const GatherJob& j : jobs) {
+        const int64_t nb = std::min<int64_t>(148 * 8, std::max<int64_t>(1, (j.out_size + 1023) / 1024));
+        gstart.push_back(gstart.back() + (int32_t)nb);
+      }
+      P.gather_blocks = gstart.back();
       TNX_CUDA(cudaMalloc(&P.d_jobs, jobs.size() * sizeof(GatherJob)));
       TNX_CUDA(cudaMemcpy(P.d_jobs, jobs.data(), jobs.size() * sizeof(GatherJob), cudaMemcpyHostToDevice));
+      TNX_CUDA(cudaMalloc(&P.d_gstart, gstart.size() * sizeof(int32_t)));
+      TNX_CUDA(cudaMemcpy(P.d_gstart, gstart.data(), gstart.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     }
     int rc = lower(P);
     if (rc) return rc;

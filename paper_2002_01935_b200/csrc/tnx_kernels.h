@@ -151,7 +151,8 @@ __device__ __forceinline__ void store_mix_x(float* plane_x, int64_t e, float v, 
 #endif
 
 // launchers (return cudaError_t)
-cudaError_t launch_gather(const GatherJob* jobs, int njobs, const float2* leaf_pool,
+cudaError_t launch_gather(const GatherJob* jobs, const int32_t* block_start, int njobs,
+                          int total_blocks, const float2* leaf_pool,
                           const unsigned long long* slice_counter, cudaStream_t st);
 cudaError_t launch_simt(const SimtParams& p, cudaStream_t st);
 // One launch for many independent thread/warp-mode SIMT contractions (one

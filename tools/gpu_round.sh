@@ -1,6 +1,6 @@
 #!/bin/bash
 # One GPU session: full GPU test suite, multi-rank smoke (gloo, shared GPU),
-# default bench, reference arm, ncu launch list + full capture of the GEMM.
+# default bench, reference arm, ncu launch list + full captures of the GEMM and the permute.
 set -u
 O=gpurun_out
 mkdir -p $O
@@ -12,3 +12,4 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 0 --ref-budget 4
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-tf32-probe"
 $CMD > $O/plain_launch.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $CMD > $O/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
 python tools/run_gemm.py 8192 8192 4096 1 2 > $O/plain_gemm.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:gemm_c64 -c 1 -o $O/prof_gemm_full python tools/run_gemm.py 8192 8192 4096 1 1 > $O/ncu_gemm.log 2>&1; echo "ncu gemm rc=$?"
+python tools/run_perm.py 3 > $O/plain_perm.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"perm|gather" -c 2 -o $O/prof_perm_full python tools/run_perm.py 1 > $O/ncu_perm.log 2>&1; echo "ncu perm rc=$?"
