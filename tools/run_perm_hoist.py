@@ -1,7 +1,6 @@
-"""Hoisted variant of run_perm.py (27 dim-2 labels, 2^27 elements, not sliced): the perm runs once at bind, so time it from an ncu launch list.
-that interleaves free and contracted labels, so packing it into the GEMM's
-K-blocked split-TF32 planes is a genuine transpose.  Prints the perm launch
-time and its algorithmic HBM bandwidth (8 B read + 16 B written per element)."""
+"""Hoisted variant of run_perm.py: x has 27 dim-2 labels (2^27 elements) with
+interleaved free / contracted labels and is not sliced, so its permute into the
+GEMM planes runs once at bind (time it from an ncu launch list)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
