@@ -87,6 +87,22 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherJob* __restrict
   const int nk = j.n_kept;
   const int64_t inner = nk > 0 ? j.kdim[nk - 1] : 1;
   const int64_t inner_st = nk > 0 ? j.kst[nk - 1] : 0;
+  if (j.vec) {  // element pairs: the inner run has unit stride and even length
+    const int64_t half = inner >> 1;
+    float4* dst4 = reinterpret_cast<float4*>(j.dst);
+    for (int64_t e = (int64_t)lb * blockDim.x + threadIdx.x; e < (j.out_size >> 1);
+         e += (int64_t)nb * blockDim.x) {
+      int64_t idx = e / half;
+      int64_t off = base + 2 * (e - idx * half);
+      for (int i = nk - 2; i >= 0; --i) {
+        const int64_t q = idx / j.kdim[i];
+        off += (idx - q * j.kdim[i]) * j.kst[i];
+        idx = q;
+      }
+      __stcs(dst4 + e, __ldcs(reinterpret_cast<const float4*>(pool + off)));
+    }
+    return;
+  }
   for (int64_t e = (int64_t)lb * blockDim.x + threadIdx.x; e < j.out_size; e += (int64_t)nb * blockDim.x) {
     int64_t idx = e / inner;
     int64_t off = base + (e - idx * inner) * inner_st;

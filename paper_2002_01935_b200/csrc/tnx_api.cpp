@@ -1269,6 +1269,13 @@ int tnx_bind_leaves(void* plan, const void* const* leaf_data, int32_t dtype, int
           j.n_kept++;
         }
       }
+      {
+        bool v = j.n_kept > 0 && j.kst[j.n_kept - 1] == 1 && j.kdim[j.n_kept - 1] % 2 == 0 && j.src % 2 == 0 &&
+                 reinterpret_cast<uintptr_t>(j.dst) % 16 == 0;
+        for (int q = 0; v && q < j.n_kept - 1; ++q) v = j.kst[q] % 2 == 0;
+        for (int q = 0; v && q < j.n_sl; ++q) v = j.sst[q] % 2 == 0;
+        j.vec = v ? 1 : 0;
+      }
       jobs.push_back(j);
     }
     P.njobs = (int)jobs.size();

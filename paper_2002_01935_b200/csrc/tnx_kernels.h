@@ -99,6 +99,8 @@ struct GatherJob {
   int64_t out_size;
   int32_t n_kept;
   int32_t n_sl;
+  int32_t vec;            // 1: inner run contiguous, even length, every base even (16 B copies)
+  int32_t pad;
   int64_t kdim[kMaxLeafRank];
   int64_t kst[kMaxLeafRank];
   uint64_t radix[kMaxLeafRank];   // suffix product of the slice dims

@@ -13,5 +13,5 @@ for name, ws in (("cfg4p_7x7_d16", 16), ("cfg4p_7x7_d20", 24), ("cfg4p_7x7_d20",
         plan.run()
         got = complex(plan.result())
         plan.close()
-        print(f"{name} ws={ws} {prec:11s} promote={os.environ.get('TNX_GEMM_PROMOTE', '4')} "
+        print(f"{name} ws={ws} {prec:11s} promote={os.environ.get('TNX_GEMM_PROMOTE', '3 (default)')} "
               f"rel_err={abs(got - ref) / abs(ref):.3e}", flush=True)

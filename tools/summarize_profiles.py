@@ -1,0 +1,160 @@
+"""Turn a gpu_round.sh session (gpurun_out/) into the tracked summaries under
+profiles/: the per-kernel launch-list shares, the GEMM and permute ncu
+full-capture summaries (time, DRAM traffic vs algorithmic bytes, pipe
+utilisation) and copies of the bench JSON lines.
+
+    python tools/summarize_profiles.py [gpurun_out] [profiles] [round tag, e.g. r01]
+"""
+import csv
+import io
+import json
+import os
+import shutil
+import subprocess
+import sys
+from collections import defaultdict
+
+SRC = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out"
+DST = sys.argv[2] if len(sys.argv) > 2 else "profiles"
+TAG = sys.argv[3] if len(sys.argv) > 3 else "r01"
+
+
+def raw_rows(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
+                         check=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    head, units = rows[0], rows[1]
+    return [dict(zip(head, r)) for r in rows[2:]], dict(zip(head, units))
+
+
+def scaled(d, units, key):
+    """Metric value in base units (bytes, seconds, Hz)."""
+    v = float(d[key])
+    u = units.get(key, "")
+    mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+            "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1,
+            "us": 1e-6, "ns": 1e-9, "ms": 1e-3, "hz": 1, "Khz": 1e3, "Mhz": 1e6, "Ghz": 1e9}
+    return v * mult.get(u, 1)
+
+
+def get(d, *keys):
+    for k in keys:
+        if k in d and d[k] not in ("", "n/a"):
+            return d[k]
+    return None
+
+
+def launches():
+    path = os.path.join(SRC, "launches.csv")
+    if not os.path.exists(path):
+        return
+    lines = [ln for ln in open(path) if ln.startswith('"')]
+    rows = list(csv.DictReader(io.StringIO("".join(lines))))
+    tot = defaultdict(float)
+    cnt = defaultdict(int)
+    for r in rows:
+        if r.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        name = r["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "").replace("tnx::", "")
+        v = float(r["Metric Value"].replace(",", ""))
+        unit = r.get("Metric Unit", "nsecond")
+        tot[name] += v * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}.get(unit, 1e-6)
+        cnt[name] += 1
+    s = sum(tot.values())
+    summ = {"command": "ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --steps 2 "
+                       "--warmup 3 --no-cpu-baseline --no-e2e --no-tf32-probe",
+            "note": "cold-cache serialised per-launch times (bind+hoist, warmup+timed slices, profile_slice); "
+                    "compare shares, not absolutes",
+            "kernels": [{"kernel": k, "launches": cnt[k], "total_ms": round(tot[k], 3),
+                         "share": round(tot[k] / s, 4)} for k in sorted(tot, key=lambda k: -tot[k])]}
+    shutil.copy(path, os.path.join(DST, f"{TAG}_launches.csv"))
+    json.dump(summ, open(os.path.join(DST, f"{TAG}_launches_summary.json"), "w"), indent=1)
+    print("launches:", [(k["kernel"], k["share"]) for k in summ["kernels"][:4]])
+
+
+def gemm():
+    rep = os.path.join(SRC, "prof_gemm_full.ncu-rep")
+    if not os.path.exists(rep):
+        return
+    rows, units = raw_rows(rep)
+    d = rows[0]
+    t = scaled(d, units, "gpu__time_duration.sum")
+    rd = scaled(d, units, "dram__bytes_read.sum")
+    wr = scaled(d, units, "dram__bytes_write.sum")
+    M = N = 8192
+    K = 4096
+    alg = 16 * (M * K + K * N) + 8 * M * N  # 4 fp32 planes of A and B + c64 output
+    flops = 8 * M * N * K
+    out = {"kernel": d["Kernel Name"],
+           "command": "ncu --set full --clock-control none --import-source on -k regex:gemm_c64 -c 1 "
+                      "python tools/run_gemm.py 8192 8192 4096 1 1",
+           "sm_clock_ghz": scaled(d, units, "sm__cycles_elapsed.avg.per_second") / 1e9,
+           "duration_ms": t * 1e3,
+           "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+           "algorithmic_bytes": alg, "traffic_over_algorithmic": (rd + wr) / alg,
+           "flops_8MNK": flops, "achieved_tflops_complex_at_ncu_clock": flops / t / 1e12,
+           "tensor_pipe_active_pct": float(get(d, "sm__pipe_tensor_op_tcgen05_cycles_active.avg.pct_of_peak_sustained_active",
+                                              "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active",
+                                              "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active") or "nan"),
+           "lts_throughput_pct": float(get(d, "lts__throughput.avg.pct_of_peak_sustained_elapsed") or "nan"),
+           "dram_throughput_pct": float(get(d, "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+                                            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed") or "nan"),
+           "registers_per_thread": int(float(d["launch__registers_per_thread"])),
+           "grid": d.get("launch__grid_size"), "cluster": "x".join(
+               d.get(f"launch__cluster_dim_{a}", "1") for a in "xyz")}
+    json.dump(out, open(os.path.join(DST, "ncu_gemm_traffic.json"), "w"), indent=1)
+    shutil.copy(rep, os.path.join(DST, f"{TAG}_gemm_full.ncu-rep"))
+    print("gemm:", round(out["duration_ms"], 3), "ms", round(out["achieved_tflops_complex_at_ncu_clock"], 1), "TF/s")
+
+
+def perm():
+    rep = os.path.join(SRC, "prof_perm_full.ncu-rep")
+    if not os.path.exists(rep):
+        return
+    rows, units = raw_rows(rep)
+    peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else None
+    ks = []
+    for d in rows:
+        t = scaled(d, units, "gpu__time_duration.sum")
+        rd = scaled(d, units, "dram__bytes_read.sum")
+        wr = scaled(d, units, "dram__bytes_write.sum")
+        name = d["Kernel Name"].split("(")[0]
+        # tools/run_perm.py: one slice of x = 4^13 complex64 elements
+        n = 4 ** 13
+        alg = 8 * n * 2 if name.startswith("gather") else 8 * n + 16 * n
+        ks.append({"kernel": name, "duration_us": t * 1e6, "dram_read": rd, "dram_write": wr,
+                   "algorithmic_bytes": alg, "achieved_gbs_algorithmic": alg / t / 1e9,
+                   "dram_gbs": (rd + wr) / t / 1e9,
+                   "frac_of_measured_hbm": (alg / t / 1e9) / peak if peak else None,
+                   "dram_active_pct": float(d.get("dram__cycles_active.avg.pct_of_peak_sustained_elapsed", "nan")),
+                   "registers_per_thread": int(float(d["launch__registers_per_thread"])),
+                   "achieved_occupancy_pct": float(d.get("sm__warps_active.avg.pct_of_peak_sustained_active", "nan")),
+                   "smem_bank_conflicts": d.get("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum")})
+    out = {"workload": "tools/run_perm.py: x[s, m0,k0,...,m5,k5,m6] (13 dim-4 labels + sliced dim-2 label) "
+                       "packed into K-blocked split-TF32 GEMM planes every slice: 2^26 complex64 in, "
+                       "4 x 2^26 fp32 out; the gather copies the slice of the sliced leaf",
+           "command": "ncu --set full --clock-control none --import-source on -k regex:'perm|gather' -c 2 "
+                      "python tools/run_perm.py 1",
+           "peak_gbs": peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write bytes)",
+           "kernels": ks}
+    json.dump(out, open(os.path.join(DST, "ncu_perm_traffic.json"), "w"), indent=1)
+    shutil.copy(rep, os.path.join(DST, f"{TAG}_perm_full.ncu-rep"))
+    print("perm:", [(k["kernel"], round(k["duration_us"], 1), round(k["achieved_gbs_algorithmic"])) for k in ks])
+
+
+def benches():
+    for src, dst in [("bench_default.log", f"{TAG}_bench_default.json"),
+                     ("bench_reference.log", f"{TAG}_bench_reference.json"),
+                     ("bench_2rank_gloo.log", f"{TAG}_bench_2rank_gloo_shared_gpu.json")]:
+        p = os.path.join(SRC, src)
+        if os.path.exists(p):
+            line = [ln for ln in open(p) if ln.startswith("{")][-1]
+            json.dump(json.loads(line), open(os.path.join(DST, dst), "w"), indent=1)
+
+
+if __name__ == "__main__":
+    os.makedirs(DST, exist_ok=True)
+    launches()
+    gemm()
+    perm()
+    benches()
