@@ -149,6 +149,20 @@ int tnx_partial_result(void* plan, double* out, int64_t out_elems, void* stream)
 /* strip_exponent plans: per output element value = out * 2^exp2. */
 int tnx_partial_result_exp(void* plan, double* out, int64_t* exp2, int64_t out_elems, void* stream);
 
+/* Single-process multi-device sum of the sliced partials (SURVEY.md §8(b)
+ * "tnx_allreduce(handles[], ndev)"; the reduction the reference's SPEC
+ * leaves to the caller, compensated per SPEC.md:551): every
+ * plan's accumulator is replaced by the sum over all `nplans` plans (Kahan sum
+ * of acc - comp in plan order, or exponent-aligned in strip_exponent mode).
+ * Plans may live on different devices (peer copies over NVLink, staged by the
+ * driver when peer access is off) or on the same one, must be bound and have
+ * the same output size and mode.  streams[i] (or NULL / streams == NULL for
+ * the library streams) orders the exchange after each plan's pending slices;
+ * returns after the exchange is enqueued (tnx_partial_result synchronises).
+ * Multi-process jobs (one process per GPU) use torch.distributed / NCCL over
+ * tnx_partial_result instead (paper_2002_01935_b200/distributed.py). */
+int tnx_allreduce(void* const* plans, int32_t nplans, void* const* streams);
+
 int tnx_stats_get(void* plan, tnx_stats* out);
 int tnx_vertex_info_get(void* plan, int32_t index, tnx_vertex_info* out);
 

@@ -72,6 +72,7 @@ SIGNATURES = {
     "tnx_debug_vertex": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int32, C.POINTER(C.c_float), C.c_int64,
                                    C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "tnx_synchronize": (C.c_int, [C.c_void_p]),
+    "tnx_allreduce": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.POINTER(C.c_void_p)]),
     "tnx_profile_slice": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                     C.POINTER(C.c_float), C.POINTER(C.c_double), C.c_int32,
                                     C.POINTER(C.c_int32)]),

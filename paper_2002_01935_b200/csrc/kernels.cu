@@ -12,6 +12,7 @@
 //               fallback; the tiled permute `perm_kernel` is the fast path).
 //  K6 accum   : root -> tn.output order, Kahan-compensated complex128
 //               accumulation across slices.
+#include <climits>
 #include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -655,6 +656,58 @@ __global__ void accum_kernel(const AccumParams p) {
 
 cudaError_t launch_accum(const AccumParams& p, cudaStream_t st) {
   accum_kernel<<<grid_for(p.out_size, 256, 148 * 8), 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+// All-reduce of n plans' accumulators gathered into one buffer ([n][out]):
+// Kahan sum of (acc_i - comp_i) (SPEC.md:551 compensated, order-fixed), or in
+// strip_exponent mode the exponent-aligned sum of acc_i * 2^exp_i.
+__global__ void allreduce_kernel(const double2* __restrict__ acc, const double2* __restrict__ comp,
+                                 const long long* __restrict__ exps, int n, int64_t out_size,
+                                 double2* out_acc, double2* out_comp, long long* out_exp) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < out_size; o += stride) {
+    if (exps) {
+      long long emax = LLONG_MIN;
+      for (int i = 0; i < n; ++i) {
+        const double2 v = acc[i * out_size + o];
+        if (v.x != 0.0 || v.y != 0.0) emax = max(emax, exps[i * out_size + o]);
+      }
+      double2 s = make_double2(0.0, 0.0);
+      if (emax != LLONG_MIN) {
+        for (int i = 0; i < n; ++i) {
+          const double2 v = acc[i * out_size + o];
+          if (v.x == 0.0 && v.y == 0.0) continue;
+          const double f = ldexp(1.0, (int)max(-1100LL, exps[i * out_size + o] - emax));
+          s.x += v.x * f;
+          s.y += v.y * f;
+        }
+      }
+      out_acc[o] = s;
+      out_exp[o] = emax == LLONG_MIN ? 0 : emax;
+      continue;
+    }
+    double2 s = make_double2(0.0, 0.0), c = make_double2(0.0, 0.0);
+    for (int t = 0; t < 2 * n; ++t) {
+      const int i = t >> 1;
+      double2 x = (t & 1) ? comp[i * out_size + o] : acc[i * out_size + o];
+      if (t & 1) x = make_double2(-x.x, -x.y);
+      const double yr = x.x - c.x, yi = x.y - c.y;
+      const double tr = s.x + yr, ti = s.y + yi;
+      c.x = (tr - s.x) - yr;
+      c.y = (ti - s.y) - yi;
+      s = make_double2(tr, ti);
+    }
+    out_acc[o] = s;
+    out_comp[o] = c;
+  }
+}
+
+cudaError_t launch_allreduce(const double2* acc, const double2* comp, const long long* exps, int n,
+                             int64_t out_size, double2* out_acc, double2* out_comp, long long* out_exp,
+                             cudaStream_t st) {
+  allreduce_kernel<<<grid_for(out_size, 256, 148 * 8), 256, 0, st>>>(acc, comp, exps, n, out_size, out_acc,
+                                                                    out_comp, out_exp);
   return cudaGetLastError();
 }
 

@@ -168,6 +168,8 @@ struct Plan {
   Int2Off* d_tabs = nullptr;
   GatherJob* d_jobs = nullptr;
   int32_t* d_gstart = nullptr;
+  void* ar_buf = nullptr;      // tnx_allreduce gather buffer (root plan)
+  int64_t ar_bytes = 0;
   int njobs = 0;
   int gather_blocks = 0;
   double2* acc = nullptr;
@@ -208,7 +210,7 @@ struct Plan {
     gexec = nullptr;
     graph = nullptr;
     void* ptrs[] = {pool,    work,   persist, partial, d_tabs,    d_jobs,   acc,    comp,
-                    counter, d_ptabs, d_bjobs, d_bstarts, d_absmax, d_exps, d_acc_exp, d_gstart};
+                    counter, d_ptabs, d_bjobs, d_bstarts, d_absmax, d_exps, d_acc_exp, d_gstart, ar_buf};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     pool = nullptr;
@@ -223,6 +225,8 @@ struct Plan {
     d_acc_exp = nullptr;
     d_jobs = nullptr;
     d_gstart = nullptr;
+    ar_buf = nullptr;
+    ar_bytes = 0;
     acc = comp = nullptr;
     counter = nullptr;
     if (own) cudaStreamDestroy(own);
@@ -1424,6 +1428,92 @@ int tnx_partial_result_exp(void* plan, double* out, int64_t* exp2, int64_t out_e
   TNX_CUDA(cudaMemcpyAsync(out, P.acc, P.out_size * 16, cudaMemcpyDeviceToHost, st));
   TNX_CUDA(cudaMemcpyAsync(exp2, P.d_acc_exp, P.out_size * 8, cudaMemcpyDeviceToHost, st));
   TNX_CUDA(cudaStreamSynchronize(st));
+  return TNX_OK;
+}
+
+int tnx_allreduce(void* const* plans, int32_t nplans, void* const* streams) {
+  if (!plans || nplans < 1) return fail(TNX_ERR_INVALID, "tnx_allreduce: no plans");
+  for (int i = 0; i < nplans; ++i) {
+    if (!plans[i]) return fail(TNX_ERR_INVALID, "tnx_allreduce: null plan");
+    for (int j = 0; j < i; ++j)
+      if (plans[j] == plans[i]) return fail(TNX_ERR_INVALID, "tnx_allreduce: plan listed twice");
+  }
+  Plan& R = *static_cast<Plan*>(plans[0]);
+  for (int i = 0; i < nplans; ++i) {
+    const Plan& P = *static_cast<const Plan*>(plans[i]);
+    if (!P.bound) return fail(TNX_ERR_STATE, "tnx_allreduce: plan " + std::to_string(i) + " not bound");
+    if (P.out_size != R.out_size || P.strip() != R.strip())
+      return fail(TNX_ERR_INVALID, "tnx_allreduce: plans differ in output size or strip_exponent mode");
+  }
+  auto stream_of = [&](int i) {
+    Plan& P = *static_cast<Plan*>(plans[i]);
+    return streams && streams[i] ? static_cast<cudaStream_t>(streams[i]) : P.own;
+  };
+  int prev = 0;
+  TNX_CUDA(cudaGetDevice(&prev));
+  const int n = nplans;
+  const int64_t out = R.out_size;
+  const bool strip = R.strip();
+  const int64_t vbytes = out * 16, ebytes = out * 8;
+  const int64_t need = (int64_t)n * (strip ? vbytes + ebytes : 2 * vbytes);
+  cudaStream_t s0 = stream_of(0);
+  TNX_CUDA(cudaSetDevice(R.device));
+  if (R.ar_bytes < need) {
+    if (R.ar_buf) TNX_CUDA(cudaFree(R.ar_buf));
+    R.ar_buf = nullptr;
+    TNX_CUDA(cudaMalloc(&R.ar_buf, need));
+    R.ar_bytes = need;
+  }
+  char* buf = static_cast<char*>(R.ar_buf);
+  double2* g_acc = reinterpret_cast<double2*>(buf);
+  double2* g_comp = strip ? nullptr : reinterpret_cast<double2*>(buf + n * vbytes);
+  long long* g_exp = strip ? reinterpret_cast<long long*>(buf + n * vbytes) : nullptr;
+  std::vector<cudaEvent_t> evs(n, nullptr);
+  auto cleanup = [&]() {
+    for (int i = 0; i < n; ++i)
+      if (evs[i]) {
+        cudaSetDevice(static_cast<Plan*>(plans[i])->device);
+        cudaEventDestroy(evs[i]);
+      }
+    cudaSetDevice(prev);
+  };
+  auto copy = [&](void* dst, int ddev, const void* src, int sdev, int64_t bytes) {
+    return ddev == sdev ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s0)
+                        : cudaMemcpyPeerAsync(dst, ddev, src, sdev, bytes, s0);
+  };
+  cudaError_t e = cudaSuccess;
+  // 1. order after every plan's pending work, gather its partial into the root buffer
+  for (int i = 0; i < n && e == cudaSuccess; ++i) {
+    Plan& P = *static_cast<Plan*>(plans[i]);
+    e = cudaSetDevice(P.device);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&evs[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(evs[i], stream_of(i));
+    if (e == cudaSuccess) e = cudaSetDevice(R.device);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s0, evs[i], 0);
+    if (e == cudaSuccess) e = copy(g_acc + i * out, R.device, P.acc, P.device, vbytes);
+    if (e == cudaSuccess && strip) e = copy(g_exp + i * out, R.device, P.d_acc_exp, P.device, ebytes);
+    if (e == cudaSuccess && !strip) e = copy(g_comp + i * out, R.device, P.comp, P.device, vbytes);
+  }
+  // 2. reduce on the root device into the root's accumulator
+  if (e == cudaSuccess) e = cudaSetDevice(R.device);
+  if (e == cudaSuccess)
+    e = launch_allreduce(g_acc, g_comp, g_exp, n, out, R.acc, strip ? nullptr : R.comp,
+                         strip ? R.d_acc_exp : nullptr, s0);
+  // 3. broadcast the total back; every plan's stream waits for the exchange
+  for (int i = 1; i < n && e == cudaSuccess; ++i) {
+    Plan& P = *static_cast<Plan*>(plans[i]);
+    e = copy(P.acc, P.device, R.acc, R.device, vbytes);
+    if (e == cudaSuccess && strip) e = copy(P.d_acc_exp, P.device, R.d_acc_exp, R.device, ebytes);
+    if (e == cudaSuccess && !strip) e = copy(P.comp, P.device, R.comp, R.device, vbytes);
+  }
+  if (e == cudaSuccess) e = cudaEventRecord(evs[0], s0);
+  for (int i = 1; i < n && e == cudaSuccess; ++i) {
+    e = cudaSetDevice(static_cast<Plan*>(plans[i])->device);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(stream_of(i), evs[0], 0);
+  }
+  // events may be destroyed once recorded/waited on (resources are released on completion)
+  cleanup();
+  if (e != cudaSuccess) return fail(TNX_ERR_CUDA, std::string("tnx_allreduce: ") + cudaGetErrorString(e));
   return TNX_OK;
 }
 

@@ -167,6 +167,9 @@ cudaError_t launch_pack(const PackParams& p, cudaStream_t st);
 cudaError_t launch_perm(const PermParams& p, cudaStream_t st);
 cudaError_t launch_dot(const DotParams& p, cudaStream_t st);
 cudaError_t launch_accum(const AccumParams& p, cudaStream_t st);
+cudaError_t launch_allreduce(const double2* acc, const double2* comp, const long long* exps, int n,
+                             int64_t out_size, double2* out_acc, double2* out_comp, long long* out_exp,
+                             cudaStream_t st);
 cudaError_t launch_set_counter(unsigned long long* counter, unsigned long long v, cudaStream_t st);
 cudaError_t launch_convert_c128(const double2* src, float2* dst, int64_t n, cudaStream_t st);
 cudaError_t launch_zero(void* p, int64_t bytes, cudaStream_t st);

@@ -29,7 +29,7 @@ from . import _native as nat
 from .network import DataError, TensorNetwork, TensorNode
 
 __all__ = ["SlicedPlan", "contract", "contract_sliced", "amplitude", "AmplitudeEngine",
-           "PRECISIONS"]
+           "allreduce_plans", "PRECISIONS"]
 
 PRECISIONS = {"fp32": nat.PREC_FP32, "3xtf32": nat.PREC_3XTF32, "tf32-bf16x": nat.PREC_TF32_BF16X}
 DEFAULT_PRECISION = "3xtf32"
@@ -339,6 +339,21 @@ def _slice_range(d, slice_ids):
     return int(s0), int(s1)
 
 
+def allreduce_plans(plans, streams=None):
+    """Sum the accumulators of bound plans (one process, any devices) on the
+    device through ``tnx_allreduce``; afterwards every plan holds the total."""
+    plans = list(plans)
+    if not plans:
+        raise ValueError("no plans")
+    lib = plans[0]._lib
+    hs = (C.c_void_p * len(plans))(*[p._h.value if isinstance(p._h, C.c_void_p) else p._h for p in plans])
+    sts = None
+    if streams is not None:
+        sts = (C.c_void_p * len(plans))(*[SlicedPlan._stream(s).value if s is not None else None
+                                          for s in streams])
+    nat.check(lib.tnx_allreduce(hs, len(plans), sts))
+
+
 def contract_sliced(tn, tree, slice_set=(), options=None, *, slice_ids=None, devices=(0,),
                     precision=None, graph=True, hoist=True):
     """Sum over slice assignments of the per-slice contraction.
@@ -361,14 +376,12 @@ def contract_sliced(tn, tree, slice_set=(), options=None, *, slice_ids=None, dev
         G = len(plans)
         bounds = [s0 + (s1 - s0) * g // G for g in range(G + 1)]
         errs = [None] * G
-        parts = [None] * G
 
         def work(g):
             try:
                 p = plans[g]
                 p.bind()
                 p.run(bounds[g], bounds[g + 1])
-                parts[g] = p.result_exp() if strip else p.result()
             except BaseException as exc:  # noqa: BLE001
                 errs[g] = exc
 
@@ -383,14 +396,13 @@ def contract_sliced(tn, tree, slice_set=(), options=None, *, slice_ids=None, dev
         for e in errs:
             if e is not None:
                 raise e
+        if G > 1:
+            allreduce_plans(plans)
         ops = plans[0].ops_per_slice * (s1 - s0)
         if strip:
-            val, exp10 = _combine_exp(parts, tn)
+            val, exp10 = _combine_exp([plans[0].result_exp()], tn)
             return val, exp10, ops
-        total = parts[0]
-        for p in parts[1:]:
-            total = total + p
-        val, exp10 = _finish(total, tn, strip)
+        val, exp10 = _finish(plans[0].result(), tn, strip)
         return val, exp10, ops
     finally:
         for p in plans:

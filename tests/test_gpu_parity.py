@@ -416,3 +416,55 @@ def test_large_sliced_leaves_gather():
     ref, _, _ = oracle.contract_sliced(tn, tree, S)
     assert rel_err(plan.result(), ref) <= TOL
     plan.close()
+
+
+def test_allreduce_plans_on_one_device():
+    """tnx_allreduce over three plans (same GPU) holding disjoint slice blocks:
+    every plan ends with the total, equal to the oracle's full sliced sum."""
+    from paper_2002_01935_b200.executor import allreduce_plans
+    tn = gen.grid_circuit(4, 4, 12, seed=3)
+    tree = best_greedy_tree(tn, trials=2)
+    ss = greedy_slice(tree, tn, metrics(tree, tn).width - 3, restarts=1)
+    plans = [SlicedPlan(tn, tree, ss).bind() for _ in range(3)]
+    try:
+        d = plans[0].d
+        assert d >= 3
+        cuts = [0, d // 3, 2 * d // 3, d]
+        for g, p in enumerate(plans):
+            p.run(cuts[g], cuts[g + 1])
+        allreduce_plans(plans)
+        ref, _, _ = oracle.contract_sliced(tn, tree, ss.labels)
+        vals = [p.result() for p in plans]
+        for v in vals:
+            assert rel_err(v, ref) <= TOL
+        assert all(np.array_equal(vals[0], v) for v in vals[1:])
+        # mismatched output size is refused
+        tn2, tree2 = _two_tensor_net(["a", "b"], ["b", "c"], ["a", "c"])
+        other = SlicedPlan(tn2, tree2, ()).bind()
+        try:
+            assert other.stats()["out_elements"] == 4 != plans[0].stats()["out_elements"]
+            with pytest.raises(ValueError, match="output size"):
+                allreduce_plans([plans[0], other])
+        finally:
+            other.close()
+    finally:
+        for p in plans:
+            p.close()
+
+
+@pytest.mark.parametrize("strip", [False, True])
+def test_contract_sliced_device_list_sums_on_device(strip):
+    """contract_sliced(devices=(0, 0)): two plans, one host thread each, the
+    partials summed by tnx_allreduce (plain and strip_exponent modes)."""
+    tn = gen.grid_circuit(4, 4, 12, seed=5)
+    tree = best_greedy_tree(tn, trials=2)
+    ss = greedy_slice(tree, tn, metrics(tree, tn).width - 2, restarts=1)
+    opts = {"strip_exponent": strip}
+    v2, e2, ops2 = contract_sliced(tn, tree, ss, opts, devices=(0, 0))
+    v1, e1, ops1 = contract_sliced(tn, tree, ss, opts, devices=(0,))
+    ref, _, _ = oracle.contract_sliced(tn, tree, ss.labels)
+    assert ops1 == ops2 == ss.Cs
+    got2 = np.asarray(v2) * 10.0 ** e2
+    got1 = np.asarray(v1) * 10.0 ** e1
+    assert rel_err(got2, ref) <= TOL and rel_err(got1, ref) <= TOL
+    assert rel_err(got2, got1) <= 1e-12

@@ -125,3 +125,24 @@ def test_auto_slice_fits_budget():
     small, need_small = auto_slice(tree, tn, 4 << 20)
     assert need_small <= 0.9 * (4 << 20) and small.Ws <= big.Ws
     assert small.Cs >= big.Cs
+
+
+def test_allreduce_argument_checks():
+    """tnx_allreduce error behaviour needs no device: empty list, duplicate
+    plan and unbound plans are refused with ValueError (no CUDA call made)."""
+    from paper_2002_01935_b200.executor import allreduce_plans
+    tn = gen.random_regular(12, 3, seed=1)
+    from paper_2002_01935_b200.harness.paths import greedy_tree
+    tree = greedy_tree(tn, seed=0)
+    a = SlicedPlan(tn, tree, ())
+    b = SlicedPlan(tn, tree, ())
+    try:
+        with pytest.raises(ValueError):
+            allreduce_plans([])
+        with pytest.raises(ValueError, match="twice"):
+            allreduce_plans([a, a])
+        with pytest.raises(ValueError, match="not bound"):
+            allreduce_plans([a, b])
+    finally:
+        a.close()
+        b.close()
