@@ -182,6 +182,8 @@ struct GemmArgs {
   float* dplanes;
   int64_t dplane_stride;
   IdxMap fmap, gmap;
+  int32_t debug;         // TNX_GEMM_DEBUG bit 0: skip the TMA loads (MMA-pipeline ceiling; wrong results)
+  int32_t pad_;
 };
 
 __device__ __forceinline__ int64_t map_offset(const IdxMap& m, int64_t idx) {
@@ -463,6 +465,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(smem_addr(&empty[stage]), phase ^ 1u);
           const uint32_t fb = smem_addr(&full[stage]);
+          if (g.debug & 1) {
+            if (leader) mbar_expect_tx(fb, 0);
+            if (++stage == C::NSTAGE) {
+              stage = 0;
+              phase ^= 1u;
+            }
+            continue;
+          }
           if (leader) mbar_expect_tx(fb, (TWO_SM ? 2 : 1) * C::STAGE);
           unsigned char* sbase = smem + stage * C::STAGE;
           const int kbg = kb_begin + kb;
@@ -702,16 +712,69 @@ int encode_planes(void* tmap, const float* base, int64_t rows_total, int64_t kp,
 }  // namespace
 
 // 2-CTA pairs for tall GEMMs with enough pair tiles (TNX_GEMM_2SM=0 disables).
-int gemm_use_2sm(int64_t batch, int64_t M, int64_t N, int64_t kp) {
-  static int mode = -1;
+// Launch configuration cost model: pick (2-CTA pairs or single CTAs, split-K
+// factor) minimising  waves * k-blocks per unit * t_kb  + split-K traffic,
+// where waves = ceil(units / slots) over the 74 SM pairs / 148 SMs.  t_kb
+// per slot: 2-CTA 256x128 tiles at full per-SM efficiency, 1-CTA 128x128 tiles
+// at 0.88 of it (measured tensor-pipe 76 % vs 83-92 %).  Split-K adds the
+// partials' HBM round trip ((2s+1) * M*N*8 B) and needs >= 8 k-blocks per unit,
+// an even output size and a workspace <= 1 GB.  TNX_GEMM_2SM=0 forces 1-CTA.
+namespace {
+struct GemmConfig {
+  int two_sm;
+  int splits;
+};
+GemmConfig gemm_best_config(int64_t batch, int64_t M, int64_t N, int64_t kp, int fixed_splits) {
+  static int mode = -1, model = -1;
   if (mode < 0) {
     const char* e = getenv("TNX_GEMM_2SM");
     mode = e ? atoi(e) : 1;
+    const char* m = getenv("TNX_GEMM_MODEL");
+    model = m ? atoi(m) : 1;
   }
-  if (!mode) return 0;
-  (void)kp;
-  const int64_t pair_tiles = ((M + 255) / 256) * ((N + BN - 1) / BN) * batch;
-  return M >= 256 && pair_tiles >= 74 ? 1 : 0;
+  if (!model) {  // previous heuristics (A/B comparisons)
+    const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * batch;
+    int sp = 1;
+    if (tiles < 148) sp = (int)std::max<int64_t>(1, std::min<int64_t>(148 / tiles, kp / BK / 8));
+    if (fixed_splits > 0) sp = fixed_splits;
+    const int64_t pair_tiles = ((M + 255) / 256) * ((N + BN - 1) / BN) * batch;
+    return {mode && M >= 256 && pair_tiles >= 74 ? 1 : 0, sp};
+  }
+  const int64_t nkb = kp / BK;
+  const double r_sm = 2.0e12;                // complex flop/s per SM (~296 TF/s / 148)
+  const double hbm = 5.0e12;                 // B/s for the split-K partials
+  const double per_wave = 1.0e-6;            // pipeline fill / epilogue tail per wave
+  const bool even = (batch * M * N) % 2 == 0;
+  GemmConfig best{0, 1};
+  double best_t = 1e300;
+  for (int t = 0; t <= 1; ++t) {
+    if (t && (!mode || M < 256)) continue;
+    const int64_t tiles = (t ? (M + 255) / 256 : (M + BM - 1) / BM) * ((N + BN - 1) / BN) * batch;
+    const int64_t slots = t ? 74 : 148;
+    const double tkb = 8.0 * (t ? 256 : BM) * BN * BK / (t ? 2.0 * r_sm : 0.88 * r_sm);
+    // enough splits to fill two waves (few output tiles, long K), >= 8 k-blocks each
+    const int64_t sfill = std::max<int64_t>(16, (2 * slots + tiles - 1) / tiles);
+    const int smax = fixed_splits > 0 ? fixed_splits : (int)std::max<int64_t>(1, std::min(sfill, nkb / 8));
+    for (int sp = fixed_splits > 0 ? fixed_splits : 1; sp <= smax; ++sp) {
+      if (sp > 1 && (!even || 8.0 * sp * batch * M * N > 1.0e9)) break;
+      const int64_t kbu = (nkb + sp - 1) / sp;
+      const int64_t zs = (nkb + kbu - 1) / kbu;
+      const int64_t units = tiles * zs;
+      const int64_t waves = (units + slots - 1) / slots;
+      double time = (double)waves * ((double)kbu * tkb + per_wave);
+      if (zs > 1) time += (2.0 * zs + 1.0) * 8.0 * batch * M * N / hbm;
+      if (time < best_t * (1.0 - 1e-9)) {
+        best_t = time;
+        best = {t, (int)zs};
+      }
+    }
+  }
+  return best;
+}
+}  // namespace
+
+int gemm_use_2sm(int64_t batch, int64_t M, int64_t N, int64_t kp, int splits) {
+  return gemm_best_config(batch, M, N, kp, splits > 0 ? splits : 1).two_sm;
 }
 
 int gemm_init_attributes(char* err, size_t errlen) {
@@ -745,7 +808,7 @@ int gemm_prepare(GemmPlan* g, const float* a_planes, const float* b_planes, floa
     snprintf(err, errlen, "gemm: row coordinate exceeds int32");
     return 1;
   }
-  g->two_sm = gemm_use_2sm(batch, M, N, kp);
+  g->two_sm = gemm_use_2sm(batch, M, N, kp, splits);
   if (encode_planes(g->tmap_a, a_planes, batch * M, kp, BM, err, errlen)) return 1;
   if (encode_planes(g->tmap_b, b_planes, batch * N, kp, g->two_sm ? BN_HALF : BN, err, errlen))
     return 1;
@@ -775,12 +838,7 @@ __global__ void splitk_reduce_kernel(const float4* __restrict__ part, float4* __
 }
 
 int gemm_choose_splits(int64_t batch, int64_t M, int64_t N, int64_t kp) {
-  const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * batch;
-  const int64_t nkb = kp / BK;
-  if (tiles >= 148) return 1;
-  int64_t s = 148 / tiles;
-  s = std::min<int64_t>(s, nkb / 8);  // at least 8 k-blocks (K=128) per CTA
-  return (int)std::max<int64_t>(1, s);
+  return gemm_best_config(batch, M, N, kp, 0).splits;
 }
 
 // k-blocks (of 16) accumulated in TMEM per promotion round; TNX_GEMM_PROMOTE
@@ -825,6 +883,11 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
   a.fmap = g.fmap;
   a.gmap = g.gmap;
   a.group_m = gemm_group_m();
+  {
+    static const int dbg = getenv("TNX_GEMM_DEBUG") ? atoi(getenv("TNX_GEMM_DEBUG")) : 0;
+    a.debug = dbg;
+    a.pad_ = 0;
+  }
   const int splits = g.splits > 1 ? g.splits : 1;
   a.kb_per_split = (a.num_kb + splits - 1) / splits;
   a.partial = splits > 1 ? g.partial : nullptr;

@@ -204,7 +204,7 @@ int gemm_prepare(GemmPlan* g, const float* a_planes, const float* b_planes, floa
                  int64_t batch, int64_t M, int64_t N, int64_t kp, int splits, float2* partial,
                  char* err, size_t errlen);
 int gemm_choose_splits(int64_t batch, int64_t M, int64_t N, int64_t kp);
-int gemm_use_2sm(int64_t batch, int64_t M, int64_t N, int64_t kp);
+int gemm_use_2sm(int64_t batch, int64_t M, int64_t N, int64_t kp, int splits);
 cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st);
 int gemm_init_attributes(char* err, size_t errlen);
 
