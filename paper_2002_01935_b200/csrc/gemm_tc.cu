@@ -209,19 +209,23 @@ __device__ __forceinline__ int64_t map_offset(const IdxMap& m, int64_t idx) {
 // four split-TF32 planes of the parent GEMM operand, column offsets from the
 // per-CTA table `gtab` (built by the epilogue warps once the main loop is
 // done and the pipeline's shared memory is free).
+// EPI: 0 interleaved complex64 (or split-K partials), 1 direct planes (scalar
+// stores), 2 direct planes in float4 runs (scalar fallback for edge tiles).
+// Templated so each kernel instance carries only its own store code.
+template <int EPI, bool MIX>
 __device__ __forceinline__ void epilogue_store(const GemmArgs& g, float2* out, int64_t grow,
                                                bool row_ok, int64_t col0, int hcol,
                                                const float (&mre)[64], const float (&mim)[64],
                                                const int64_t* gtab) {
   if (!row_ok) return;
-  if (g.direct && g.dvec && col0 + 64 <= g.N) {
+  if (EPI == 2 && col0 + 64 <= g.N) {
     const int64_t f = map_offset(g.fmap, grow);
     float* d = g.dplanes;
     const int64_t ps = g.dplane_stride;
 #pragma unroll
     for (int j = 0; j < 64; j += 4) {
       const int64_t off = f + gtab[hcol + j];
-      if (g.dmix) {
+      if constexpr (MIX) {
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           d[off + t] = tf32_hi(mre[j + t]);
@@ -246,7 +250,7 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& g, float2* out, i
     }
     return;
   }
-  if (g.direct) {
+  if constexpr (EPI >= 1) {
     const int64_t f = map_offset(g.fmap, grow);
     float* d = g.dplanes;
     const int64_t ps = g.dplane_stride;
@@ -259,7 +263,7 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& g, float2* out, i
       const float ih = __uint_as_float(__float_as_uint(im) & 0xffffe000u);
       d[off] = rh;
       d[off + 2 * ps] = ih;
-      if (g.dmix) {
+      if constexpr (MIX) {
         store_mix_x(d + ps, off, re, g.dside);
         store_mix_x(d + 3 * ps, off, im, g.dside);
       } else {
@@ -397,7 +401,7 @@ __device__ __forceinline__ void decode_unit(const GemmArgs& g, int u, int& z, in
   tn = (t % group_span) / gm;
 }
 
-template <bool TWO_SM>
+template <bool TWO_SM, bool MIX, int EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_c64_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a,
                            const __grid_constant__ CUtensorMap tm_b, const GemmArgs g) {
@@ -536,7 +540,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const uint64_t bi_h = umma_desc_sw64(bb + 2 * C::B_BYTES);
               const uint64_t bi_l = umma_desc_sw64(bb + 3 * C::B_BYTES);
               const uint32_t acc0 = (kb > kb0 || ks > 0) ? 1u : 0u;
-              if (g.mix) {
+              if constexpr (MIX) {
                 // planes: 0 re_hi (tf32), 1 re_x (bf16 [hi|lo] / [lo|hi]), 2 im_hi, 3 im_x
                 if constexpr (TWO_SM) {
                   umma_bf16_2sm(d_re, ar_l, br_l, ID_BP, acc0);
@@ -643,14 +647,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       float2* const out = g.partial ? g.partial + (int64_t)z * g.batch * g.M * g.N : g.out;
       const int64_t row = (int64_t)tm * C::TILE_M + rank * BM + q * 32 + lane;
-      if (g.direct) {
+      if constexpr (EPI >= 1) {
         asm volatile("bar.sync 1, 256;" ::: "memory");  // previous unit's stores done with gtab
         const int e = threadIdx.x - 64;
         const int64_t cb = (int64_t)tn * BN;
         if (e < BN) gtab[e] = (cb + e < g.N) ? map_offset(g.gmap, cb + e) : 0;
         asm volatile("bar.sync 1, 256;" ::: "memory");
       }
-      epilogue_store(g, out, (int64_t)b * g.M + row, row < g.M, (int64_t)tn * BN + h * 64, h * 64, mre,
+      epilogue_store<EPI, MIX>(g, out, (int64_t)b * g.M + row, row < g.M, (int64_t)tn * BN + h * 64, h * 64, mre,
                      mim, gtab);
     }
   }
@@ -777,12 +781,30 @@ int gemm_use_2sm(int64_t batch, int64_t M, int64_t N, int64_t kp, int splits) {
   return gemm_best_config(batch, M, N, kp, splits > 0 ? splits : 1).two_sm;
 }
 
+typedef void (*GemmKernelFn)(CUtensorMap, CUtensorMap, GemmArgs);
+
+template <bool TWO_SM>
+GemmKernelFn gemm_kernel_for(bool mix, int epi) {
+  if (mix) {
+    if (epi == 2) return gemm_c64_3xtf32_kernel<TWO_SM, true, 2>;
+    if (epi == 1) return gemm_c64_3xtf32_kernel<TWO_SM, true, 1>;
+    return gemm_c64_3xtf32_kernel<TWO_SM, true, 0>;
+  }
+  if (epi == 2) return gemm_c64_3xtf32_kernel<TWO_SM, false, 2>;
+  if (epi == 1) return gemm_c64_3xtf32_kernel<TWO_SM, false, 1>;
+  return gemm_c64_3xtf32_kernel<TWO_SM, false, 0>;
+}
+
 int gemm_init_attributes(char* err, size_t errlen) {
-  cudaError_t e = cudaFuncSetAttribute(gemm_c64_3xtf32_kernel<true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, KCfg<true>::SMEM);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(gemm_c64_3xtf32_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             KCfg<false>::SMEM);
+  cudaError_t e = cudaSuccess;
+  for (int mix = 0; mix < 2 && e == cudaSuccess; ++mix)
+    for (int epi = 0; epi < 3 && e == cudaSuccess; ++epi) {
+      e = cudaFuncSetAttribute(gemm_kernel_for<true>(mix, epi), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               KCfg<true>::SMEM);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(gemm_kernel_for<false>(mix, epi), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 KCfg<false>::SMEM);
+    }
   if (e != cudaSuccess) {
     snprintf(err, errlen, "cudaFuncSetAttribute(gemm): %s", cudaGetErrorString(e));
     return 1;
@@ -897,6 +919,8 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
   a.splits = zs;
   const CUtensorMap* ta = reinterpret_cast<const CUtensorMap*>(g.tmap_a);
   const CUtensorMap* tb = reinterpret_cast<const CUtensorMap*>(g.tmap_b);
+  const int epi = a.direct ? (a.dvec ? 2 : 1) : 0;
+  if (g.direct && g.dmix != g.mix) return cudaErrorInvalidValue;  // planes follow the plan's precision
   if (g.two_sm) a.tiles_m = (int32_t)((g.M + 255) / 256);
   const int64_t units = (int64_t)a.tiles_m * a.tiles_n * g.batch * zs;
   cudaLaunchConfig_t cfg = {};
@@ -913,12 +937,12 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t le = cudaLaunchKernelEx(&cfg, gemm_c64_3xtf32_kernel<true>, *ta, *tb, a);
+    cudaError_t le = cudaLaunchKernelEx(&cfg, gemm_kernel_for<true>(a.mix != 0, epi), *ta, *tb, a);
     if (le != cudaSuccess) return le;
   } else {
     cfg.gridDim = dim3((unsigned)std::min<int64_t>(units, 148));
     cfg.dynamicSmemBytes = KCfg<false>::SMEM;
-    cudaError_t le = cudaLaunchKernelEx(&cfg, gemm_c64_3xtf32_kernel<false>, *ta, *tb, a);
+    cudaError_t le = cudaLaunchKernelEx(&cfg, gemm_kernel_for<false>(a.mix != 0, epi), *ta, *tb, a);
     if (le != cudaSuccess) return le;
   }
   cudaError_t e = cudaGetLastError();

@@ -1245,7 +1245,6 @@ int tnx_bind_leaves(void* plan, const void* const* leaf_data, int32_t dtype, int
     for (int i : P.gather_leaves) {
       GatherJob j{};
       const std::vector<int>& ls = P.leaf_labels[i];
-      if ((int)ls.size() > kMaxLeafRank) return fail(TNX_ERR_INVALID, "leaf rank exceeds 16");
       j.src = P.pool_off[i];
       j.dst = reinterpret_cast<float2*>(P.block_ptr(1, P.T[i].block));
       j.out_size = P.T[i].size;
@@ -1257,6 +1256,10 @@ int tnx_bind_leaves(void* plan, const void* const* leaf_data, int32_t dtype, int
       }
       for (size_t q = 0; q < ls.size(); ++q) {
         int l = ls[q];
+        const bool merge = P.slice_pos[l] < 0 && j.n_kept > 0 && j.kst[j.n_kept - 1] == st[q] * P.dims[l];
+        if (!merge && (P.slice_pos[l] >= 0 ? j.n_sl : j.n_kept) >= kMaxLeafRank)
+          return fail(TNX_ERR_INVALID, "leaf " + std::to_string(i) + ": more than " + std::to_string(kMaxLeafRank) +
+                                           " sliced labels or non-contiguous kept runs");
         if (P.slice_pos[l] >= 0) {
           u128 rad = 1;
           for (size_t t = P.slice_pos[l] + 1; t < P.sliced.size(); ++t) rad *= (u128)P.dims[P.sliced[t]];
@@ -1264,7 +1267,7 @@ int tnx_bind_leaves(void* plan, const void* const* leaf_data, int32_t dtype, int
           j.sdim[j.n_sl] = P.dims[l];
           j.sst[j.n_sl] = st[q];
           j.n_sl++;
-        } else if (j.n_kept > 0 && j.kst[j.n_kept - 1] == st[q] * P.dims[l]) {
+        } else if (merge) {
           j.kdim[j.n_kept - 1] *= P.dims[l];  // merge into the previous contiguous run
           j.kst[j.n_kept - 1] = st[q];
         } else {

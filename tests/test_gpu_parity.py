@@ -468,3 +468,22 @@ def test_contract_sliced_device_list_sums_on_device(strip):
     got1 = np.asarray(v1) * 10.0 ** e1
     assert rel_err(got2, ref) <= TOL and rel_err(got1, ref) <= TOL
     assert rel_err(got2, got1) <= 1e-12
+
+
+def test_high_rank_sliced_leaf():
+    """A rank-21 leaf carrying a sliced label (kept labels merge into two
+    contiguous runs, so the gather's 16-run limit is not hit)."""
+    from paper_2002_01935_b200.tree import ContractionTree
+    rng = np.random.default_rng(11)
+    al = [f"a{i}" for i in range(10)]
+    bl = [f"b{i}" for i in range(10)]
+    tab = {l: 2 for l in al + bl + ["s", "c"]}
+    xl = al[:5] + ["s"] + al[5:] + bl          # rank 21, s in the middle
+    yl = bl + ["s", "c"]
+    x = ((rng.standard_normal((2,) * 21) + 1j * rng.standard_normal((2,) * 21)) / 32).astype(np.complex128)
+    y = ((rng.standard_normal((2,) * 12) + 1j * rng.standard_normal((2,) * 12)) / 32).astype(np.complex128)
+    tn = TensorNetwork([TensorNode(0, xl, x), TensorNode(1, yl, y)], tab, tuple(al + ["c"]))
+    tree = ContractionTree((0, 1), [(0, 1)])
+    got, _, _ = contract_sliced(tn, tree, ("s",))
+    ref, _, _ = oracle.contract_sliced(tn, tree, ("s",))
+    assert rel_err(got, ref) <= TOL
