@@ -177,6 +177,8 @@ struct Plan {
   unsigned long long* counter = nullptr;
   cudaStream_t own = nullptr;
   cudaGraph_t graph = nullptr;
+  cudaGraph_t hgraph = nullptr;       // hoisted phase (replayed by every re-bind)
+  cudaGraphExec_t hgexec = nullptr;
   cudaGraphExec_t gexec = nullptr;
   std::vector<Launch> hoist_launches, slice_launches;
   std::vector<SimtParams> simt;
@@ -207,8 +209,12 @@ struct Plan {
   void release() {
     if (gexec) cudaGraphExecDestroy(gexec);
     if (graph) cudaGraphDestroy(graph);
+    if (hgexec) cudaGraphExecDestroy(hgexec);
+    if (hgraph) cudaGraphDestroy(hgraph);
     gexec = nullptr;
     graph = nullptr;
+    hgexec = nullptr;
+    hgraph = nullptr;
     void* ptrs[] = {pool,    work,   persist, partial, d_tabs,    d_jobs,   acc,    comp,
                     counter, d_ptabs, d_bjobs, d_bstarts, d_absmax, d_exps, d_acc_exp, d_gstart, ar_buf};
     for (void* p : ptrs)
@@ -1359,9 +1365,30 @@ int tnx_bind_leaves(void* plan, const void* const* leaf_data, int32_t dtype, int
     }
   }
   (void)max_leaf;
-  // hoisted (slice-invariant) subtrees, computed once
-  int rc = run_launches(P, P.hoist_launches, st, -1);
-  if (rc) return rc;
+  // hoisted (slice-invariant) subtrees, computed once per bind; captured as a
+  // graph on the first bind (fixed buffers) and replayed by later re-binds
+  int rc = 0;
+  if (!(P.flags & TNX_FLAG_NO_GRAPH) && !P.hoist_launches.empty()) {
+    if (!P.hgexec) {
+      cudaStream_t cs = P.own;
+      TNX_CUDA(cudaStreamSynchronize(st));
+      TNX_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      rc = run_launches(P, P.hoist_launches, cs, -1);
+      cudaGraph_t g = nullptr;
+      cudaError_t ce = cudaStreamEndCapture(cs, &g);
+      if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      if (ce != cudaSuccess) return fail(TNX_ERR_CUDA, std::string("hoist graph capture: ") + cudaGetErrorString(ce));
+      P.hgraph = g;
+      TNX_CUDA(cudaGraphInstantiate(&P.hgexec, g, 0));
+    }
+    TNX_CUDA(cudaGraphLaunch(P.hgexec, st));
+  } else {
+    rc = run_launches(P, P.hoist_launches, st, -1);
+    if (rc) return rc;
+  }
   TNX_CUDA(cudaMemsetAsync(P.acc, 0, std::max<int64_t>(P.out_size, 1) * 16, st));
   TNX_CUDA(cudaMemsetAsync(P.comp, 0, std::max<int64_t>(P.out_size, 1) * 16, st));
   if (P.d_acc_exp) TNX_CUDA(cudaMemsetAsync(P.d_acc_exp, 0, std::max<int64_t>(P.out_size, 1) * 8, st));
