@@ -183,7 +183,7 @@ struct GemmArgs {
   int64_t dplane_stride;
   IdxMap fmap, gmap;
   int32_t debug;         // TNX_GEMM_DEBUG bit 0: skip the TMA loads (MMA-pipeline ceiling; wrong results)
-  int32_t pad_;
+  int32_t dstack;        // direct planes of a stacked-B parent operand: also write -im_hi, -im_lo (planes 4, 5)
 };
 
 __device__ __forceinline__ int64_t map_offset(const IdxMap& m, int64_t idx) {
@@ -247,6 +247,10 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& g, float2* out, i
       *reinterpret_cast<float4*>(d + off + ps) = make_float4(rl[0], rl[1], rl[2], rl[3]);
       *reinterpret_cast<float4*>(d + off + 2 * ps) = make_float4(ih[0], ih[1], ih[2], ih[3]);
       *reinterpret_cast<float4*>(d + off + 3 * ps) = make_float4(il[0], il[1], il[2], il[3]);
+      if (g.dstack) {
+        *reinterpret_cast<float4*>(d + off + 4 * ps) = make_float4(-ih[0], -ih[1], -ih[2], -ih[3]);
+        *reinterpret_cast<float4*>(d + off + 5 * ps) = make_float4(-il[0], -il[1], -il[2], -il[3]);
+      }
     }
     return;
   }
@@ -269,6 +273,10 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& g, float2* out, i
       } else {
         d[off + ps] = re - rh;
         d[off + 3 * ps] = im - ih;
+        if (g.dstack) {
+          d[off + 4 * ps] = -ih;
+          d[off + 5 * ps] = ih - im;
+        }
       }
     }
     return;
@@ -321,12 +329,19 @@ constexpr int NUM_THREADS = 320;
 constexpr int BN_HALF = BN / 2;
 constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;
 
-template <bool TWO_SM>
+// STACK (2-CTA, 3xTF32 only): "stacked B".  Each CTA stages four full
+// 128-row B slots, CTA0 {re_hi, re_lo, -im_hi, -im_lo} and CTA1 {im_hi,
+// im_lo, re_hi, re_lo}, so one N=256 MMA A_re x [B_re | B_im] (slots 0/1) and
+// one A_im x [-B_im | B_re] (slots 2/3) accumulate straight into the
+// [Re | Im] TMEM columns: 12 MMAs of N=256 per k-block instead of 24 of N=128,
+// shared-memory operand traffic per k-block 144 + 48 KB -> 96 + 64 KB.  The B
+// operand carries two extra planes (-im_hi, -im_lo; planes 4, 5).
+template <bool TWO_SM, bool STACK = false>
 struct KCfg {
-  static constexpr int A_BYTES = BM * BK * 4;                          // 8 KB
-  static constexpr int B_BYTES = (TWO_SM ? BN_HALF : BN) * BK * 4;     // 4 / 8 KB
-  static constexpr int STAGE = 4 * A_BYTES + 4 * B_BYTES;              // 48 / 64 KB
-  static constexpr int NSTAGE = TWO_SM ? 4 : 3;
+  static constexpr int A_BYTES = BM * BK * 4;                                        // 8 KB
+  static constexpr int B_BYTES = (TWO_SM && !STACK ? BN_HALF : BN) * BK * 4;         // 4 / 8 KB
+  static constexpr int STAGE = 4 * A_BYTES + 4 * B_BYTES;                            // 48 / 64 KB
+  static constexpr int NSTAGE = TWO_SM && !STACK ? 4 : 3;
   static constexpr int GTAB_OFF = NSTAGE * STAGE;                      // 1 KB column table
   static constexpr int BAR_OFF = GTAB_OFF + BN * 8;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
@@ -381,9 +396,9 @@ __device__ __forceinline__ void mbar_arrive_leader(uint32_t local_addr) {
 // idesc: D=f32, A=B=tf32 (fmt 2) or bf16 (fmt 1), K-major, N=128, M=128 (1 CTA)
 // or 256 (pair)
 template <bool TWO_SM>
-__host__ __device__ constexpr uint32_t idesc_mma(bool neg_a, uint32_t fmt = 2u) {
+__host__ __device__ constexpr uint32_t idesc_mma(bool neg_a, uint32_t fmt = 2u, int n = BN) {
   return (1u << 4) | (fmt << 7) | (fmt << 10) | ((neg_a ? 1u : 0u) << 13) |
-         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((TWO_SM ? 256 : BM) >> 4) << 24);
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)((TWO_SM ? 256 : BM) >> 4) << 24);
 }
 
 // work unit -> (split z, batch b, tile row tm, tile column tn)
@@ -401,11 +416,12 @@ __device__ __forceinline__ void decode_unit(const GemmArgs& g, int u, int& z, in
   tn = (t % group_span) / gm;
 }
 
-template <bool TWO_SM, bool MIX, int EPI>
+template <bool TWO_SM, bool MIX, int EPI, bool STACK>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_c64_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a,
                            const __grid_constant__ CUtensorMap tm_b, const GemmArgs g) {
-  using C = KCfg<TWO_SM>;
+  static_assert(!STACK || (TWO_SM && !MIX), "stacked B is a 2-CTA 3xTF32 variant");
+  using C = KCfg<TWO_SM, STACK>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -465,7 +481,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int kb_begin = z * g.kb_per_split;
         const int nkb = min(g.num_kb - kb_begin, g.kb_per_split);
         const int row_a = (int)(b * g.M + (int64_t)tm * C::TILE_M + rank * BM);
-        const int row_b = (int)(b * g.N + (int64_t)tn * BN + rank * BN_HALF);
+        const int row_b = (int)(b * g.N + (int64_t)tn * BN + (STACK ? 0 : rank * BN_HALF));
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(smem_addr(&empty[stage]), phase ^ 1u);
           const uint32_t fb = smem_addr(&full[stage]);
@@ -482,7 +498,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int kbg = kb_begin + kb;
 #pragma unroll
           for (int p = 0; p < 4; ++p) {
-            if constexpr (TWO_SM) {
+            if constexpr (STACK) {
+              // B slot p of this CTA: CTA0 planes {0, 1, 4, 5}, CTA1 {2, 3, 0, 1}
+              const int bp = rank == 0 ? (p < 2 ? p : p + 2) : (p < 2 ? p + 2 : p - 2);
+              tma_load_3d_2sm(smem_addr(sbase + p * C::A_BYTES), &tm_a, fb, 0, row_a, p * g.num_kb + kbg);
+              tma_load_3d_2sm(smem_addr(sbase + 4 * C::A_BYTES + p * C::B_BYTES), &tm_b, fb, 0, row_b,
+                              bp * g.num_kb + kbg);
+            } else if constexpr (TWO_SM) {
               tma_load_3d_2sm(smem_addr(sbase + p * C::A_BYTES), &tm_a, fb, 0, row_a, p * g.num_kb + kbg);
               tma_load_3d_2sm(smem_addr(sbase + 4 * C::A_BYTES + p * C::B_BYTES), &tm_b, fb, 0, row_b,
                               p * g.num_kb + kbg);
@@ -506,6 +528,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       constexpr uint32_t ID_NEG = idesc_mma<TWO_SM>(true);
       constexpr uint32_t ID_BP = idesc_mma<TWO_SM>(false, 1u);
       constexpr uint32_t ID_BN = idesc_mma<TWO_SM>(true, 1u);
+      constexpr uint32_t ID_S = idesc_mma<TWO_SM>(false, 2u, 2 * BN);  // N = 256 (stacked B)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t R = 0;  // global accumulator-round counter
@@ -540,6 +563,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const uint64_t bi_h = umma_desc_sw64(bb + 2 * C::B_BYTES);
               const uint64_t bi_l = umma_desc_sw64(bb + 3 * C::B_BYTES);
               const uint32_t acc0 = (kb > kb0 || ks > 0) ? 1u : 0u;
+              if constexpr (STACK) {
+                // slots: 0 [re_hi | im_hi], 1 [re_lo | im_lo], 2 [-im_hi | re_hi], 3 [-im_lo | re_lo]
+                umma_tf32_2sm(d_re, ar_h, br_l, ID_S, acc0);  // hi.lo
+                umma_tf32_2sm(d_re, ar_l, br_h, ID_S, 1u);    // lo.hi
+                umma_tf32_2sm(d_re, ai_h, bi_l, ID_S, 1u);
+                umma_tf32_2sm(d_re, ai_l, bi_h, ID_S, 1u);
+                umma_tf32_2sm(d_re, ar_h, br_h, ID_S, 1u);    // hi.hi
+                umma_tf32_2sm(d_re, ai_h, bi_h, ID_S, 1u);
+                continue;
+              }
               if constexpr (MIX) {
                 // planes: 0 re_hi (tf32), 1 re_x (bf16 [hi|lo] / [lo|hi]), 2 im_hi, 3 im_x
                 if constexpr (TWO_SM) {
@@ -692,12 +725,12 @@ EncodeTiledFn get_encode(char* err, size_t errlen) {
 }
 
 int encode_planes(void* tmap, const float* base, int64_t rows_total, int64_t kp, int box_rows,
-                  char* err, size_t errlen) {
+                  char* err, size_t errlen, int nplanes = 4) {
   EncodeTiledFn enc = get_encode(err, errlen);
   if (!enc) return 1;
   // K-blocked planes [plane][kp/16][rows][16]: every box is one contiguous
   // block of box_rows x 64 B (rows past `rows` are zero-filled).
-  cuuint64_t dims[3] = {(cuuint64_t)BK, (cuuint64_t)rows_total, (cuuint64_t)(4 * (kp / BK))};
+  cuuint64_t dims[3] = {(cuuint64_t)BK, (cuuint64_t)rows_total, (cuuint64_t)(nplanes * (kp / BK))};
   cuuint64_t strides[2] = {(cuuint64_t)(BK * 4), (cuuint64_t)(rows_total * BK * 4)};
   cuuint32_t box[3] = {(cuuint32_t)BK, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
@@ -777,6 +810,22 @@ GemmConfig gemm_best_config(int64_t batch, int64_t M, int64_t N, int64_t kp, int
 }
 }  // namespace
 
+int gemm_stack_enabled() {
+  static const int v = getenv("TNX_GEMM_STACKB") ? atoi(getenv("TNX_GEMM_STACKB")) : 1;
+  return v;
+}
+
+// Stacked B pays when its MMA-time gain (~13 % of 8*M*N*K at ~300 TF/s,
+// measured) exceeds the extra B-plane traffic (+8 B written by the producer
+// and +8 B read per B element, ~16*N*K bytes at ~5 TB/s):  M > ~920 rows.
+// Streaming-bound shapes (few A rows, e.g. M=256 with K=2^19) stay unstacked.
+int gemm_use_stack(int64_t batch, int64_t M, int64_t N, int64_t kp, int two_sm) {
+  (void)batch;
+  (void)N;
+  (void)kp;
+  return two_sm && gemm_stack_enabled() && M >= 1024 ? 1 : 0;
+}
+
 int gemm_use_2sm(int64_t batch, int64_t M, int64_t N, int64_t kp, int splits) {
   return gemm_best_config(batch, M, N, kp, splits > 0 ? splits : 1).two_sm;
 }
@@ -784,15 +833,22 @@ int gemm_use_2sm(int64_t batch, int64_t M, int64_t N, int64_t kp, int splits) {
 typedef void (*GemmKernelFn)(CUtensorMap, CUtensorMap, GemmArgs);
 
 template <bool TWO_SM>
-GemmKernelFn gemm_kernel_for(bool mix, int epi) {
-  if (mix) {
-    if (epi == 2) return gemm_c64_3xtf32_kernel<TWO_SM, true, 2>;
-    if (epi == 1) return gemm_c64_3xtf32_kernel<TWO_SM, true, 1>;
-    return gemm_c64_3xtf32_kernel<TWO_SM, true, 0>;
+GemmKernelFn gemm_kernel_for(bool mix, int epi, bool stack = false) {
+  if constexpr (TWO_SM) {
+    if (stack && !mix) {
+      if (epi == 2) return gemm_c64_3xtf32_kernel<true, false, 2, true>;
+      if (epi == 1) return gemm_c64_3xtf32_kernel<true, false, 1, true>;
+      return gemm_c64_3xtf32_kernel<true, false, 0, true>;
+    }
   }
-  if (epi == 2) return gemm_c64_3xtf32_kernel<TWO_SM, false, 2>;
-  if (epi == 1) return gemm_c64_3xtf32_kernel<TWO_SM, false, 1>;
-  return gemm_c64_3xtf32_kernel<TWO_SM, false, 0>;
+  if (mix) {
+    if (epi == 2) return gemm_c64_3xtf32_kernel<TWO_SM, true, 2, false>;
+    if (epi == 1) return gemm_c64_3xtf32_kernel<TWO_SM, true, 1, false>;
+    return gemm_c64_3xtf32_kernel<TWO_SM, true, 0, false>;
+  }
+  if (epi == 2) return gemm_c64_3xtf32_kernel<TWO_SM, false, 2, false>;
+  if (epi == 1) return gemm_c64_3xtf32_kernel<TWO_SM, false, 1, false>;
+  return gemm_c64_3xtf32_kernel<TWO_SM, false, 0, false>;
 }
 
 int gemm_init_attributes(char* err, size_t errlen) {
@@ -804,6 +860,9 @@ int gemm_init_attributes(char* err, size_t errlen) {
       if (e == cudaSuccess)
         e = cudaFuncSetAttribute(gemm_kernel_for<false>(mix, epi), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  KCfg<false>::SMEM);
+      if (e == cudaSuccess && !mix)
+        e = cudaFuncSetAttribute(gemm_kernel_for<true>(false, epi, true),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, KCfg<true, true>::SMEM);
     }
   if (e != cudaSuccess) {
     snprintf(err, errlen, "cudaFuncSetAttribute(gemm): %s", cudaGetErrorString(e));
@@ -814,7 +873,7 @@ int gemm_init_attributes(char* err, size_t errlen) {
 
 int gemm_prepare(GemmPlan* g, const float* a_planes, const float* b_planes, float2* out,
                  int64_t batch, int64_t M, int64_t N, int64_t kp, int splits, float2* partial,
-                 char* err, size_t errlen) {
+                 char* err, size_t errlen, int stack_b) {
   std::memset(g, 0, sizeof(*g));
   g->splits = splits;
   g->partial = partial;
@@ -831,8 +890,14 @@ int gemm_prepare(GemmPlan* g, const float* a_planes, const float* b_planes, floa
     return 1;
   }
   g->two_sm = gemm_use_2sm(batch, M, N, kp, splits);
+  if (stack_b && !g->two_sm) {
+    snprintf(err, errlen, "gemm: stacked B needs the 2-CTA configuration");
+    return 1;
+  }
+  g->stackb = stack_b ? 1 : 0;
   if (encode_planes(g->tmap_a, a_planes, batch * M, kp, BM, err, errlen)) return 1;
-  if (encode_planes(g->tmap_b, b_planes, batch * N, kp, g->two_sm ? BN_HALF : BN, err, errlen))
+  if (encode_planes(g->tmap_b, b_planes, batch * N, kp, g->two_sm && !stack_b ? BN_HALF : BN, err, errlen,
+                    stack_b ? 6 : 4))
     return 1;
   g->out = out;
   g->M = M;
@@ -908,7 +973,7 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
   {
     static const int dbg = getenv("TNX_GEMM_DEBUG") ? atoi(getenv("TNX_GEMM_DEBUG")) : 0;
     a.debug = dbg;
-    a.pad_ = 0;
+    a.dstack = g.dstack;
   }
   const int splits = g.splits > 1 ? g.splits : 1;
   a.kb_per_split = (a.num_kb + splits - 1) / splits;
@@ -931,6 +996,7 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
   const CUtensorMap* tb = reinterpret_cast<const CUtensorMap*>(g.tmap_b);
   const int epi = a.direct ? (a.dvec ? 2 : 1) : 0;
   if (g.direct && g.dmix != g.mix) return cudaErrorInvalidValue;  // planes follow the plan's precision
+  if (g.stackb && (g.mix || !g.two_sm)) return cudaErrorInvalidValue;
   if (g.two_sm) a.tiles_m = (int32_t)((g.M + 255) / 256);
   const int64_t units = (int64_t)a.tiles_m * a.tiles_n * g.batch * zs;
   cudaLaunchConfig_t cfg = {};
@@ -940,14 +1006,14 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
   if (g.two_sm) {
     const int64_t clusters = std::min<int64_t>(units, 74);
     cfg.gridDim = dim3((unsigned)(2 * clusters));
-    cfg.dynamicSmemBytes = KCfg<true>::SMEM;
+    cfg.dynamicSmemBytes = g.stackb ? KCfg<true, true>::SMEM : KCfg<true>::SMEM;
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t le = cudaLaunchKernelEx(&cfg, gemm_kernel_for<true>(a.mix != 0, epi), *ta, *tb, a);
+    cudaError_t le = cudaLaunchKernelEx(&cfg, gemm_kernel_for<true>(a.mix != 0, epi, g.stackb != 0), *ta, *tb, a);
     if (le != cudaSuccess) return le;
   } else {
     cfg.gridDim = dim3((unsigned)std::min<int64_t>(units, 148));

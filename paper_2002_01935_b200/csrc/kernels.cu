@@ -369,6 +369,10 @@ __global__ void __launch_bounds__(256) pack_kernel(const PackParams p) {
     } else {
       p.dst[e + p.plane_stride] = re - re_hi;
       p.dst[e + 3 * p.plane_stride] = im - im_hi;
+      if (p.nplanes == 6) {  // stacked-B operand: negated imaginary planes
+        p.dst[e + 4 * p.plane_stride] = -im_hi;
+        p.dst[e + 5 * p.plane_stride] = im_hi - im;
+      }
     }
   }
 }
@@ -528,6 +532,10 @@ __global__ void __launch_bounds__(256, 4) perm_vec_kernel(const PermParams p) {
         } else {
           *reinterpret_cast<float2*>(d + off + p.plane_stride) = make_float2(v.x - ar, v.z - br);
           *reinterpret_cast<float2*>(d + off + 3 * p.plane_stride) = make_float2(v.y - ai, v.w - bi);
+          if (p.mode == 2) {  // stacked-B operand: negated imaginary planes
+            *reinterpret_cast<float2*>(d + off + 4 * p.plane_stride) = make_float2(-ai, -bi);
+            *reinterpret_cast<float2*>(d + off + 5 * p.plane_stride) = make_float2(ai - v.y, bi - v.w);
+          }
         }
       }
     }

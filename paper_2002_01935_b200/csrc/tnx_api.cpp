@@ -113,6 +113,8 @@ struct Vertex {
   int64_t chunk = 0;
   int blk_apl = -1, blk_bpl = -1, blk_part = -1, blk_tmp = -1;
   int splits = 1;
+  int two_sm = 0;                   // 2-CTA GEMM configuration
+  bool stack = false;               // stacked-B variant (B planes carry -im_hi, -im_lo)
   bool swap = false;  // GEMM A operand taken from y (larger row count)
   int direct_parent = -1;           // GEMM writes the parent's operand planes
   int direct_side = -1;
@@ -609,9 +611,11 @@ int compile(Plan& P, const tnx_plan_desc* D) {
     }
     if (v.kind == VK_GEMM) {
       const int64_t ra = v.swap ? v.N : v.M, rb = v.swap ? v.M : v.N;
-      v.blk_apl = add_block(ph, 16 * v.B * ra * v.kp, st, st);
-      v.blk_bpl = add_block(ph, 16 * v.B * rb * v.kp, st, st);
       v.splits = ((v.B * v.M * v.N) % 2 == 0) ? gemm_choose_splits(v.B, ra, rb, v.kp) : 1;
+      v.two_sm = gemm_use_2sm(v.B, ra, rb, v.kp, v.splits);
+      v.stack = P.precision == TNX_PREC_3XTF32 && gemm_use_stack(v.B, ra, rb, v.kp, v.two_sm);
+      v.blk_apl = add_block(ph, 16 * v.B * ra * v.kp, st, st);
+      v.blk_bpl = add_block(ph, (v.stack ? 24 : 16) * v.B * rb * v.kp, st, st);
       if (v.splits > 1) v.blk_part = add_block(ph, 8 * (int64_t)v.splits * v.B * v.M * v.N, st, st);
     }
   }
@@ -633,8 +637,11 @@ int compile(Plan& P, const tnx_plan_desc* D) {
     auto refresh = [&](Vertex& v) {  // derived sizes after a swap / reorder
       const int ph = v.hoisted ? 0 : 1;
       const int64_t ra = v.swap ? v.N : v.M, rb = v.swap ? v.M : v.N;
+      // the launch configuration follows the orientation (A rows pair up in 2-CTA mode)
+      v.two_sm = gemm_use_2sm(v.B, ra, rb, v.kp, v.splits);
+      v.stack = P.precision == TNX_PREC_3XTF32 && gemm_use_stack(v.B, ra, rb, v.kp, v.two_sm);
       P.blocks[ph][v.blk_apl].bytes = align_up(16 * v.B * ra * v.kp, kAlign);
-      P.blocks[ph][v.blk_bpl].bytes = align_up(16 * v.B * rb * v.kp, kAlign);
+      P.blocks[ph][v.blk_bpl].bytes = align_up((v.stack ? 24 : 16) * v.B * rb * v.kp, kAlign);
       TensorLoc& z = P.T[v.ssa];
       z.labels = v.bl;
       const std::vector<int>& f1 = v.swap ? v.nl : v.ml;
@@ -767,9 +774,9 @@ int compile(Plan& P, const tnx_plan_desc* D) {
         info += " cols_inner_strides=";
         for (int i = std::max(0, (int)f2.size() - 6); i < (int)f2.size(); ++i) info += std::to_string(pst[f2[i]]) + ",";
       }
-      fprintf(stderr, "gemm v=%d M=%lld N=%lld K=%lld swap=%d splits=%d parent=%d side=%d%s\n", v.ssa,
-              (long long)v.M, (long long)v.N, (long long)v.K, (int)v.swap, v.splits, v.direct_parent,
-              v.direct_side, info.c_str());
+      fprintf(stderr, "gemm v=%d M=%lld N=%lld K=%lld swap=%d splits=%d 2sm=%d stack=%d parent=%d side=%d%s\n",
+              v.ssa, (long long)v.M, (long long)v.N, (long long)v.K, (int)v.swap, v.splits, v.two_sm,
+              (int)v.stack, v.direct_parent, v.direct_side, info.c_str());
     }
   }
   P.persist_bytes = std::max<int64_t>(persist_off, kAlign);
@@ -992,7 +999,8 @@ int lower(Plan& P) {
             int64_t toff = 0;
             const size_t mark = P.ptabs.size();
             const bool mixp = P.precision == TNX_PREC_TF32_BF16X;
-            if (build_perm(P, src, dst, mixp ? (side == 0 ? 3 : 4) : 1, pp, toff, err)) {
+            const int pmode = mixp ? (side == 0 ? 3 : 4) : (side == 1 && v.stack ? 2 : 1);
+            if (build_perm(P, src, dst, pmode, pp, toff, err)) {
               pp.src = P.ptr(src);
               pp.dst = planes;
               pp.plane_stride = nrows * v.kp;
@@ -1015,7 +1023,7 @@ int lower(Plan& P) {
             pk.K = v.K;
             pk.kp = v.kp;
             pk.plane_stride = nrows * v.kp;
-            pk.nplanes = 4;
+            pk.nplanes = side == 1 && v.stack ? 6 : 4;
             pk.mix = P.precision == TNX_PREC_TF32_BF16X ? (side == 0 ? 1 : 2) : 0;
             P.packs.push_back(pk);
             out.push_back({L_PACK, (int)P.packs.size() - 1, v.ssa});
@@ -1023,8 +1031,11 @@ int lower(Plan& P) {
         }
         GemmPlan g;
         float2* part = v.splits > 1 ? reinterpret_cast<float2*>(P.block_ptr(phase, v.blk_part)) : nullptr;
-        if (gemm_prepare(&g, apl, bpl, P.ptr(z), v.B, ra, rb, v.kp, v.splits, part, ebuf, sizeof(ebuf)))
+        if (gemm_prepare(&g, apl, bpl, P.ptr(z), v.B, ra, rb, v.kp, v.splits, part, ebuf, sizeof(ebuf),
+                         v.stack ? 1 : 0))
           return fail(TNX_ERR_CUDA, std::string("vertex ") + std::to_string(v.ssa) + ": " + ebuf);
+        if (g.two_sm != v.two_sm)
+          return fail(TNX_ERR_INVALID, "vertex " + std::to_string(v.ssa) + ": GEMM configuration changed");
         g.mix = P.precision == TNX_PREC_TF32_BF16X ? 1 : 0;
         if (v.direct_parent >= 0) {
           const Vertex& pv = P.V[v.direct_parent - P.n];
@@ -1043,6 +1054,7 @@ int lower(Plan& P) {
           g.direct = 1;
           g.dmix = g.mix;
           g.dside = v.direct_side;
+          g.dstack = v.direct_side == 1 && pv.stack ? 1 : 0;
           g.dplanes = reinterpret_cast<float*>(
               P.block_ptr(phase, v.direct_side == 0 ? pv.blk_apl : pv.blk_bpl));
           g.dplane_stride = prows * pv.kp;
@@ -1671,10 +1683,10 @@ int tnx_profile_slice(void* plan, uint64_t s, int32_t* types, int32_t* vertices,
       double b = 0.0;
       if (L.type == L_PERM) {
         const PermParams& pp = P.perms[L.idx];
-        b = (double)pp.n_outer * pp.ts * (pp.mode == 0 ? 16.0 : 24.0);
+        b = (double)pp.n_outer * pp.ts * (pp.mode == 0 ? 16.0 : pp.mode == 2 ? 32.0 : 24.0);
       } else if (L.type == L_PACK) {
         const PackParams& pk = P.packs[L.idx];
-        b = (double)pk.rows * pk.K * 8.0 + (double)pk.rows * pk.kp * 16.0;
+        b = (double)pk.rows * pk.K * 8.0 + (double)pk.rows * pk.kp * 4.0 * pk.nplanes;
       } else if (L.type == L_DOT) {
         b = (double)P.dots[L.idx].n * 16.0;
       }
@@ -1703,8 +1715,10 @@ int tnx_gemm_c64(const void* A, const void* B, void* C, int64_t batch, int64_t M
   if (gemm_init_attributes(ebuf, sizeof(ebuf))) return fail(TNX_ERR_CUDA, ebuf);
   const int64_t kp = align_up(K, 16);
   float *apl = nullptr, *bpl = nullptr;
+  int splits = ((batch * M * N) % 2 == 0) ? gemm_choose_splits(batch, M, N, kp) : 1;
+  const bool stack = precision == TNX_PREC_3XTF32 && gemm_use_stack(batch, M, N, kp, gemm_use_2sm(batch, M, N, kp, splits));
   TNX_CUDA(cudaMalloc(&apl, 16 * batch * M * kp));
-  TNX_CUDA(cudaMalloc(&bpl, 16 * batch * N * kp));
+  TNX_CUDA(cudaMalloc(&bpl, (stack ? 24 : 16) * batch * N * kp));
   auto simple = [&](IdxMap& m, int64_t rows, int64_t stride) {
     std::memset(&m, 0, sizeof(m));
     m.n = 1;
@@ -1731,16 +1745,16 @@ int tnx_gemm_c64(const void* A, const void* B, void* C, int64_t batch, int64_t M
   pb.K = K;
   pb.kp = kp;
   pb.plane_stride = pb.rows * kp;
-  pb.nplanes = 4;
+  pb.nplanes = stack ? 6 : 4;
   pb.mix = precision == TNX_PREC_TF32_BF16X ? 2 : 0;
   cudaError_t e = launch_pack(pa, st);
   if (e == cudaSuccess) e = launch_pack(pb, st);
   if (e != cudaSuccess) return fail(TNX_ERR_CUDA, cudaGetErrorString(e));
   GemmPlan g;
-  int splits = ((batch * M * N) % 2 == 0) ? gemm_choose_splits(batch, M, N, kp) : 1;
   float2* part = nullptr;
   if (splits > 1) TNX_CUDA(cudaMalloc(&part, 8 * (size_t)splits * batch * M * N));
-  if (gemm_prepare(&g, apl, bpl, static_cast<float2*>(C), batch, M, N, kp, splits, part, ebuf, sizeof(ebuf)))
+  if (gemm_prepare(&g, apl, bpl, static_cast<float2*>(C), batch, M, N, kp, splits, part, ebuf, sizeof(ebuf),
+                   stack ? 1 : 0))
     return fail(TNX_ERR_CUDA, ebuf);
   g.mix = precision == TNX_PREC_TF32_BF16X ? 1 : 0;
   e = launch_gemm(g, st);

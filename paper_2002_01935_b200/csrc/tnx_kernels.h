@@ -192,6 +192,8 @@ struct GemmPlan {
   int32_t mix;            // mixed TF32/BF16 mode (operand planes and MMA sequence)
   int32_t dmix;           // direct planes in the mixed format for parent side dside
   int32_t dside;
+  int32_t stackb;         // stacked-B 2-CTA variant: B planes carry -im_hi, -im_lo (6 planes)
+  int32_t dstack;         // direct planes of a stacked-B parent's B operand (write 6 planes)
   int32_t pad2;
   float* dplanes;
   int64_t dplane_stride;
@@ -202,9 +204,13 @@ struct GemmPlan {
 // multiple of 16.
 int gemm_prepare(GemmPlan* g, const float* a_planes, const float* b_planes, float2* out,
                  int64_t batch, int64_t M, int64_t N, int64_t kp, int splits, float2* partial,
-                 char* err, size_t errlen);
+                 char* err, size_t errlen, int stack_b = 0);
 int gemm_choose_splits(int64_t batch, int64_t M, int64_t N, int64_t kp);
 int gemm_use_2sm(int64_t batch, int64_t M, int64_t N, int64_t kp, int splits);
+// stacked-B 2-CTA variant enabled (TNX_GEMM_STACKB=0 disables)
+int gemm_stack_enabled();
+// stacked B for this shape (cost model; requires the 2-CTA configuration)
+int gemm_use_stack(int64_t batch, int64_t M, int64_t N, int64_t kp, int two_sm);
 cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st);
 int gemm_init_attributes(char* err, size_t errlen);
 
