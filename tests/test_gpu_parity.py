@@ -487,3 +487,61 @@ def test_high_rank_sliced_leaf():
     got, _, _ = contract_sliced(tn, tree, ("s",))
     ref, _, _ = oracle.contract_sliced(tn, tree, ("s",))
     assert rel_err(got, ref) <= TOL
+
+
+@pytest.mark.parametrize("dims", [dict(b=3, m=(4, 4, 4, 4, 4), n=(5, 5, 6), k=(3, 4, 2)),    # batched, N=150
+                                  dict(b=1, m=(2,) * 11, n=(3, 3, 3, 3, 3), k=(2,) * 6)])  # N=243 (edge tile)
+def test_stacked_b_gemm_shapes(dims):
+    """The stacked-B 2-CTA GEMM (M >= 1024 rows of A): batched hyperedge
+    labels, N not a multiple of the 128-column tile, K padded to 16."""
+    from paper_2002_01935_b200.tree import ContractionTree
+    rng = np.random.default_rng(21)
+    bl = [f"h{i}" for i in range(1)] if dims["b"] > 1 else []
+    ml = [f"m{i}" for i in range(len(dims["m"]))]
+    nl = [f"n{i}" for i in range(len(dims["n"]))]
+    kl = [f"k{i}" for i in range(len(dims["k"]))]
+    tab = dict(zip(ml, dims["m"])) | dict(zip(nl, dims["n"])) | dict(zip(kl, dims["k"]))
+    if bl:
+        tab[bl[0]] = dims["b"]
+    xl, yl = bl + ml + kl, kl[::-1] + nl + bl
+    def rnd(ls):
+        shp = [tab[l] for l in ls]
+        return (rng.standard_normal(shp) + 1j * rng.standard_normal(shp)) / np.sqrt(np.prod([tab[l] for l in kl]))
+    tn = TensorNetwork([TensorNode(0, xl, rnd(xl)), TensorNode(1, yl, rnd(yl))], tab, tuple(bl + ml + nl))
+    tree = ContractionTree((0, 1), [(0, 1)])
+    plan = SlicedPlan(tn, tree, ()).bind()
+    assert [v["kind"] for v in plan.vertex_info()] == ["gemm_tc"]
+    plan.run()
+    got = plan.result()
+    plan.close()
+    ref, _, _ = oracle.contract(tn, tree)
+    assert rel_err(got, ref) <= 2e-6
+
+
+def test_stacked_parent_fed_by_direct_children():
+    """A stacked-B parent GEMM whose B operand planes (incl. the negated
+    imaginary planes) are written by a child GEMM's epilogue, vs the
+    materialised path and the oracle."""
+    from paper_2002_01935_b200.tree import ContractionTree
+    rng = np.random.default_rng(8)
+    al = [f"a{i}" for i in range(11)]
+    kl = [f"k{i}" for i in range(7)]
+    bl = [f"b{i}" for i in range(10)]
+    jl = [f"j{i}" for i in range(5)]
+    tab = {l: 2 for l in al + kl + bl + jl}
+    def rnd(ls):
+        shp = [2] * len(ls)
+        return (rng.standard_normal(shp) + 1j * rng.standard_normal(shp)) / 2 ** (len(ls) / 4)
+    # child = y[j, b] . z[j, k] -> [b, k];  parent = x[a, k] . child[b, k] -> [a, b]
+    tn = TensorNetwork([TensorNode(0, al + kl, rnd(al + kl)), TensorNode(1, jl + bl, rnd(jl + bl)),
+                        TensorNode(2, jl + kl, rnd(jl + kl))], tab, tuple(al + bl))
+    tree = ContractionTree((0, 1, 2), [(1, 2), (0, 3)])
+    vals = []
+    for direct in (True, False):
+        plan = SlicedPlan(tn, tree, (), gemm_min_macs=2 ** 10, direct_planes=direct).bind()
+        plan.run()
+        vals.append(plan.result())
+        plan.close()
+    ref, _, _ = oracle.contract(tn, tree)
+    for v in vals:
+        assert rel_err(v, ref) <= 2e-6
