@@ -184,6 +184,8 @@ struct GemmArgs {
   IdxMap fmap, gmap;
   int32_t debug;         // TNX_GEMM_DEBUG bit 0: skip the TMA loads (MMA-pipeline ceiling; wrong results)
   int32_t dstack;        // direct planes of a stacked-B parent operand: also write -im_hi, -im_lo (planes 4, 5)
+  int32_t ksnake;        // odd waves traverse K in reverse (L2 reuse across waves)
+  int32_t pad_;
 };
 
 __device__ __forceinline__ int64_t map_offset(const IdxMap& m, int64_t idx) {
@@ -495,7 +497,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           if (leader) mbar_expect_tx(fb, (TWO_SM ? 2 : 1) * C::STAGE);
           unsigned char* sbase = smem + stage * C::STAGE;
-          const int kbg = kb_begin + kb;
+          // k-snake: odd waves of the persistent grid walk K backwards, so they
+          // start on the k-slices the previous wave (same A rows under group-M
+          // rasterisation) left in L2
+          const int kbg = kb_begin + ((g.ksnake && (((u - cid) / ncta) & 1)) ? nkb - 1 - kb : kb);
 #pragma unroll
           for (int p = 0; p < 4; ++p) {
             if constexpr (STACK) {
@@ -974,6 +979,9 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
     static const int dbg = getenv("TNX_GEMM_DEBUG") ? atoi(getenv("TNX_GEMM_DEBUG")) : 0;
     a.debug = dbg;
     a.dstack = g.dstack;
+    static const int snake = getenv("TNX_GEMM_KSNAKE") ? atoi(getenv("TNX_GEMM_KSNAKE")) : 1;
+    a.ksnake = snake;
+    a.pad_ = 0;
   }
   const int splits = g.splits > 1 ? g.splits : 1;
   a.kb_per_split = (a.num_kb + splits - 1) / splits;
