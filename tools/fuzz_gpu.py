@@ -85,7 +85,9 @@ def main():
         ref, _, _ = oracle.contract_sliced(tn, tree, S, slice_ids=ids)
         ref = np.asarray(ref)
         err = float(np.linalg.norm((got - ref).ravel()))
-        scale = max(float(np.linalg.norm(ref.ravel())), 1e-2 * abs_value(tn, tree, S, ids))
+        nref = float(np.linalg.norm(ref.ravel()))
+        absv = abs_value(tn, tree, S, ids)
+        scale = max(nref, 1e-2 * absv)
         ok = err <= 1e-5 * scale if scale > 0 else err == 0.0
         scale = scale if scale > 0 else 1.0
         cases += 1
@@ -93,7 +95,8 @@ def main():
             kinds[k] = kinds.get(k, 0) + 1
         tag = "ok  " if ok else "FAIL"
         print(f"{tag} seed {seed} W={m.width:.1f} Ws={ws} |S|={len(S)} slices={s1} prec={prec} direct={direct} "
-              f"gemm_min=2^{int(np.log2(gmin))} gemms={vk.count('gemm_tc')} rel={err / scale:.2e}", flush=True)
+              f"gemm_min=2^{int(np.log2(gmin))} gemms={vk.count('gemm_tc')} rel={err / scale:.2e} "
+              f"rel_ref={err / nref if nref else 0.0:.2e} abs/ref={absv / nref if nref else 0.0:.1e}", flush=True)
         if not ok:
             fails += 1
     print(f"{cases} cases, {fails} failures; vertex kinds seen: {kinds}")
