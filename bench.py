@@ -482,6 +482,11 @@ def main():
                 "gpu_launches": K * st["launches_per_slice"],
                 "plan": {k: st[k] for k in ("num_gemm", "num_simt", "num_hoisted", "launches_per_slice",
                                             "work_arena_bytes")},
+                # context only (vs_baseline stays null: BASELINE.json lists no published number):
+                # paper Table II, 7x7 (1+40+1), single precision on a Quadro P2000, Hyper-Par trees
+                "paper_context": ({"effective_tflops": 1.353, "hardware": "NVIDIA Quadro P2000 (3.03 TFLOP/s FP32)",
+                                   "source": "BASELINE.md §1 (PAPER.md:724-725, derived 8*C_s/t)",
+                                   "ratio": value / 1.353} if args.config == WORKLOAD else None),
                 "allreduce_ms": allreduce_ms, "setup_s": setup_s, "backend": backend if use_dist else None,
                 "prefix_sum": [complex(np.asarray(total).ravel()[0]).real, complex(np.asarray(total).ravel()[0]).imag]}
         print(json.dumps(line, default=str))
