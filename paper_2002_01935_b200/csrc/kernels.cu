@@ -124,54 +124,46 @@ cudaError_t launch_gather(const GatherJob* jobs, const int32_t* start, int njobs
 }
 
 // ------------------------------------------------------------------ simt
-__global__ void __launch_bounds__(256) simt_thread_kernel(const SimtParams p) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < p.out_size; o += stride) {
-    int64_t ox = 0, oy = 0;
-    decode2(p.out, o, ox, oy);
-    float2 acc = make_float2(0.f, 0.f);
-    if (p.sum_tab) {
-      for (int64_t j = 0; j < p.sum_size; ++j) {
-        Int2Off t = p.sum_tab[j];
-        cfma(acc, p.x[ox + t.x], p.y[oy + t.y]);
-      }
-    } else {
-      for (int64_t j = 0; j < p.sum_size; ++j) {
-        int64_t sx = ox, sy = oy;
-        decode2(p.sum, j, sx, sy);
-        cfma(acc, p.x[sx], p.y[sy]);
-      }
-    }
-    p.z[o] = acc;
-  }
-}
-
-__global__ void __launch_bounds__(256) simt_warp_kernel(const SimtParams p) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t o = warp; o < p.out_size; o += nwarps) {
-    int64_t ox = 0, oy = 0;
-    decode2(p.out, o, ox, oy);
-    float2 acc = make_float2(0.f, 0.f);
-    if (p.sum_tab) {
-      for (int64_t j = lane; j < p.sum_size; j += 32) {
-        Int2Off t = p.sum_tab[j];
-        cfma(acc, p.x[ox + t.x], p.y[oy + t.y]);
-      }
-    } else {
-      for (int64_t j = lane; j < p.sum_size; j += 32) {
-        int64_t sx = ox, sy = oy;
-        decode2(p.sum, j, sx, sy);
-        cfma(acc, p.x[sx], p.y[sy]);
+// Summed-index loop shared by the SIMT kernels: lanes lane0, lane0 + step, ...
+// of [j0, j1).  Fast path when the summed labels merge into one strided run
+// (no decode / table; unrolled so independent loads overlap).
+__device__ __forceinline__ void simt_sum(const SimtParams& p, int64_t ox, int64_t oy, int64_t j0, int64_t j1,
+                                         int64_t step, float2& acc) {
+  if (p.sum.n <= 1) {
+    const int64_t s0 = p.sum.n ? p.sum.st0[0] : 0, s1 = p.sum.n ? p.sum.st1[0] : 0;
+    const float2* __restrict__ xp = p.x + ox;
+    const float2* __restrict__ yp = p.y + oy;
+    float2 a2 = make_float2(0.f, 0.f);
+    int64_t j = j0;
+    if (step == 1 && s0 == 1 && s1 == 1 && ((ox | oy | j0) & 1) == 0) {
+      // contiguous run in both operands: 16-byte loads (two complex values)
+      for (; j + 1 < j1; j += 2) {
+        const float4 xv = __ldg(reinterpret_cast<const float4*>(xp + j));
+        const float4 yv = __ldg(reinterpret_cast<const float4*>(yp + j));
+        cfma(acc, make_float2(xv.x, xv.y), make_float2(yv.x, yv.y));
+        cfma(a2, make_float2(xv.z, xv.w), make_float2(yv.z, yv.w));
       }
     }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
-      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+    for (; j + step < j1; j += 2 * step) {
+      const float2 x0 = __ldg(xp + j * s0), y0 = __ldg(yp + j * s1);
+      const float2 x1 = __ldg(xp + (j + step) * s0), y1 = __ldg(yp + (j + step) * s1);
+      cfma(acc, x0, y0);
+      cfma(a2, x1, y1);
     }
-    if (lane == 0) p.z[o] = acc;
+    if (j < j1) cfma(acc, __ldg(xp + j * s0), __ldg(yp + j * s1));
+    acc.x += a2.x;
+    acc.y += a2.y;
+  } else if (p.sum_tab) {
+    for (int64_t j = j0; j < j1; j += step) {
+      const Int2Off t = p.sum_tab[j];
+      cfma(acc, p.x[ox + t.x], p.y[oy + t.y]);
+    }
+  } else {
+    for (int64_t j = j0; j < j1; j += step) {
+      int64_t sx = ox, sy = oy;
+      decode2(p.sum, j, sx, sy);
+      cfma(acc, p.x[sx], p.y[sy]);
+    }
   }
 }
 
@@ -183,11 +175,7 @@ __global__ void __launch_bounds__(256) simt_split_kernel(const SimtParams p) {
   int64_t ox = 0, oy = 0;
   decode2(p.out, o, ox, oy);
   float2 acc = make_float2(0.f, 0.f);
-  for (int64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
-    int64_t sx = ox, sy = oy;
-    decode2(p.sum, j, sx, sy);
-    cfma(acc, p.x[sx], p.y[sy]);
-  }
+  simt_sum(p, ox, oy, j0 + threadIdx.x, j1, blockDim.x, acc);
   __shared__ float2 red[32];
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -247,12 +235,9 @@ static int grid_for(int64_t work, int threads, int max_blocks) {
 
 cudaError_t launch_simt(const SimtParams& p, cudaStream_t st) {
   if (p.out_size == 0) return cudaSuccess;
-  const int maxb = 148 * 16;
-  if (p.mode == SIMT_THREAD) {
-    simt_thread_kernel<<<grid_for(p.out_size, 256, maxb), 256, 0, st>>>(p);
-  } else if (p.mode == SIMT_WARP) {
-    simt_warp_kernel<<<grid_for(p.out_size * 32, 256, maxb), 256, 0, st>>>(p);
-  } else {
+  // thread / warp modes run batched per dependency level (launch_simt_batch)
+  if (p.mode != SIMT_SPLIT) return cudaErrorInvalidValue;
+  {
     dim3 grid((unsigned)p.nsplit, (unsigned)p.out_size);
     simt_split_kernel<<<grid, 256, 0, st>>>(p);
     cudaError_t e = cudaGetLastError();
@@ -276,56 +261,34 @@ __global__ void __launch_bounds__(256) simt_batch_kernel(const SimtParams* __res
   const SimtParams& p = jobs[lo];
   const int lb = b - start[lo];
   const int nb = start[lo + 1] - start[lo];
-  if (p.mode == SIMT_THREAD) {
-    for (int64_t o = (int64_t)lb * blockDim.x + threadIdx.x; o < p.out_size; o += (int64_t)nb * blockDim.x) {
+  // 2^lg lanes cooperate on one output (0: thread mode, 5: warp mode); the loop
+  // is warp-uniform so the group reductions are legal shuffles
+  const int lg = p.group_lg;
+  const int G = 1 << lg;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int per_warp = 32 >> lg;
+  const int64_t w0 = ((int64_t)lb * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)nb * blockDim.x) >> 5;
+  for (int64_t base = w0 * per_warp; base < p.out_size; base += nw * per_warp) {
+    const int64_t o = base + (lane >> lg);
+    const bool valid = o < p.out_size;
+    float2 acc = make_float2(0.f, 0.f);
+    if (valid) {
       int64_t ox = 0, oy = 0;
       decode2(p.out, o, ox, oy);
-      float2 acc = make_float2(0.f, 0.f);
-      if (p.sum_tab) {
-        for (int64_t j = 0; j < p.sum_size; ++j) {
-          const Int2Off t = p.sum_tab[j];
-          cfma(acc, p.x[ox + t.x], p.y[oy + t.y]);
-        }
-      } else {
-        for (int64_t j = 0; j < p.sum_size; ++j) {
-          int64_t sx = ox, sy = oy;
-          decode2(p.sum, j, sx, sy);
-          cfma(acc, p.x[sx], p.y[sy]);
-        }
-      }
-      p.z[o] = acc;
+      simt_sum(p, ox, oy, gl, p.sum_size, G, acc);
     }
-  } else {
-    const int lane = threadIdx.x & 31;
-    const int64_t w0 = ((int64_t)lb * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)nb * blockDim.x) >> 5;
-    for (int64_t o = w0; o < p.out_size; o += nw) {
-      int64_t ox = 0, oy = 0;
-      decode2(p.out, o, ox, oy);
-      float2 acc = make_float2(0.f, 0.f);
-      for (int64_t j = lane; j < p.sum_size; j += 32) {
-        int64_t sx = ox, sy = oy;
-        if (p.sum_tab) {
-          const Int2Off t = p.sum_tab[j];
-          sx += t.x;
-          sy += t.y;
-        } else {
-          decode2(p.sum, j, sx, sy);
-        }
-        cfma(acc, p.x[sx], p.y[sy]);
-      }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
-        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
-      }
-      if (lane == 0) p.z[o] = acc;
+    for (int off = G >> 1; off > 0; off >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
     }
+    if (valid && gl == 0) p.z[o] = acc;
   }
 }
 
 int simt_blocks(const SimtParams& p) {
-  const int64_t work = p.mode == SIMT_THREAD ? p.out_size : p.out_size * 32;
+  const int64_t work = p.out_size << p.group_lg;
   int64_t b = (work + 255) / 256;
   if (b < 1) b = 1;
   if (b > 148 * 16) b = 148 * 16;

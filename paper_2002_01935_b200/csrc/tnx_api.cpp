@@ -1114,6 +1114,15 @@ int lower(Plan& P) {
         s.chunk = v.chunk;
         s.partial = P.partial;
         s.sum_tab = v.tab_off >= 0 ? P.d_tabs + v.tab_off : nullptr;
+        s.group_lg = v.kind == VK_SIMT_W ? 5 : 0;
+        if (v.kind == VK_SIMT_T && s.sum.n == 1 && v.sum_size >= 2 &&
+            (s.sum.st0[0] == 1 || s.sum.st1[0] == 1)) {
+          // the summed run is contiguous in an operand: 2^lg lanes per output read it coalesced
+          static const int gmax = getenv("TNX_SIMT_GROUP_LG") ? atoi(getenv("TNX_SIMT_GROUP_LG")) : 0;
+          int lg = 0;
+          while (lg < gmax && (int64_t(2) << lg) <= v.sum_size) ++lg;
+          s.group_lg = lg;
+        }
         if (v.kind == VK_SIMT_T || v.kind == VK_SIMT_W) {
           // one launch per dependency level for all its small contractions
           if (open_batch < 0) {

@@ -40,6 +40,8 @@ struct SimtParams {
   int64_t chunk;          // SPLIT: sum elements per block
   int32_t nsplit;
   int32_t mode;
+  int32_t group_lg;       // batched THREAD/WARP: 2^group_lg lanes per output (0 thread ... 5 warp)
+  int32_t pad;
 };
 
 // Pack a complex64 tensor into fp32 planes [re_hi, re_lo, im_hi, im_lo]

@@ -13,3 +13,4 @@ CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-tf32-p
 $CMD > $O/plain_launch.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $CMD > $O/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
 python tools/run_gemm.py 8192 8192 4096 1 2 > $O/plain_gemm.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:gemm_c64 -c 1 -o $O/prof_gemm_full python tools/run_gemm.py 8192 8192 4096 1 1 > $O/ncu_gemm.log 2>&1; echo "ncu gemm rc=$?"
 python tools/run_perm.py 3 > $O/plain_perm.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"perm|gather" -c 2 -o $O/prof_perm_full python tools/run_perm.py 1 > $O/ncu_perm.log 2>&1; echo "ncu perm rc=$?"
+python tools/run_simt.py 3 > $O/plain_simt.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"simt" -c 2 -o $O/prof_simt_full python tools/run_simt.py 1 > $O/ncu_simt.log 2>&1; echo "ncu simt rc=$?"

@@ -142,6 +142,32 @@ def perm():
     print("perm:", [(k["kernel"], round(k["duration_us"], 1), round(k["achieved_gbs_algorithmic"])) for k in ks])
 
 
+def simt():
+    rep = os.path.join(SRC, "prof_simt_full.ncu-rep")
+    if not os.path.exists(rep):
+        return
+    rows, units = raw_rows(rep)
+    peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else None
+    # tools/run_simt.py: (a) x 2^24 + y 2^4 read, 2^20 written; (b) x 2^24 + y 2^14 read, 2^10 written (complex64)
+    algs = [8 * (2 ** 24 + 2 ** 4 + 2 ** 20), 8 * (2 ** 24 + 2 ** 14 + 2 ** 10)]
+    ks = []
+    for d, alg, case in zip(rows, algs, ["skinny: 2^20 outputs x 16 terms (batched SIMT, thread mode)",
+                                         "long sums: 2^10 outputs x 2^14 terms (split mode)"]):
+        t = scaled(d, units, "gpu__time_duration.sum")
+        rd = scaled(d, units, "dram__bytes_read.sum")
+        wr = scaled(d, units, "dram__bytes_write.sum")
+        ks.append({"case": case, "kernel": d["Kernel Name"].split("(")[0], "duration_us": t * 1e6,
+                   "dram_read": rd, "dram_write": wr, "algorithmic_bytes": alg,
+                   "achieved_gbs_algorithmic": alg / t / 1e9,
+                   "frac_of_measured_hbm": (alg / t / 1e9) / peak if peak else None,
+                   "registers_per_thread": int(float(d["launch__registers_per_thread"]))})
+    out = {"command": "ncu --set full --clock-control none --import-source on -k regex:simt -c 2 "
+                      "python tools/run_simt.py 1", "peak_gbs": peak, "kernels": ks}
+    json.dump(out, open(os.path.join(DST, "ncu_simt_traffic.json"), "w"), indent=1)
+    shutil.copy(rep, os.path.join(DST, f"{TAG}_simt_full.ncu-rep"))
+    print("simt:", [(k["kernel"], round(k["duration_us"], 1), round(k["achieved_gbs_algorithmic"])) for k in ks])
+
+
 def benches():
     for src, dst in [("bench_default.log", f"{TAG}_bench_default.json"),
                      ("bench_reference.log", f"{TAG}_bench_reference.json"),
@@ -157,4 +183,5 @@ if __name__ == "__main__":
     launches()
     gemm()
     perm()
+    simt()
     benches()
