@@ -8,12 +8,12 @@ import pytest
 import oracle
 from conftest import arr_from_json, golden_cases
 from _util import case_objects, rel_err
-from paper_2002_01935_b200.executor import (SlicedPlan, contract, contract_sliced, amplitude,
+from paper_2002_01935_b200.executor import (SlicedPlan, contract, contract_sliced,
                                             AmplitudeEngine)
 from paper_2002_01935_b200.network import TensorNetwork, TensorNode
 from paper_2002_01935_b200.harness import generators as gen
 from paper_2002_01935_b200.harness.paths import best_greedy_tree, greedy_tree
-from paper_2002_01935_b200.slicing import greedy_slice, SliceSet
+from paper_2002_01935_b200.slicing import greedy_slice
 from paper_2002_01935_b200.tree import metrics
 
 pytestmark = pytest.mark.gpu

@@ -10,7 +10,7 @@ from conftest import golden_cases, load_golden, REPO
 from _util import case_objects
 from paper_2002_01935_b200 import _native as nat
 from paper_2002_01935_b200.executor import SlicedPlan
-from paper_2002_01935_b200.slicing import sliced_metrics, SliceSet
+from paper_2002_01935_b200.slicing import sliced_metrics
 from paper_2002_01935_b200.tree import ContractionTree, metrics
 from paper_2002_01935_b200.harness import generators as gen
 

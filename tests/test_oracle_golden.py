@@ -1,5 +1,4 @@
 """Pin the CPU oracle against outputs of the real reference (tests/golden)."""
-import numpy as np
 import pytest
 
 import oracle

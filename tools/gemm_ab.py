@@ -1,6 +1,6 @@
 """Per-vertex GEMM times of one cfg4 slice (profile_slice, best of 3) for the
 current process's GEMM configuration env (e.g. TNX_GEMM_MODEL=0/1)."""
-import os, sys, json
+import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2002_01935_b200.executor import SlicedPlan
 from paper_2002_01935_b200.harness.workloads import load_workload

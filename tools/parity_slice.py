@@ -1,7 +1,7 @@
 """Per-vertex parity of one slice of a benchmark workload: every slice-
 dependent intermediate from the GPU (tnx_debug_vertex) vs the CPU oracle
 (complex128), norm-wise.  Usage: python tools/parity_slice.py [config] [slice] [ws]"""
-import sys, os, time, math
+import sys, os, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import oracle

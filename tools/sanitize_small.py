@@ -7,9 +7,6 @@ import oracle
 from paper_2002_01935_b200.executor import SlicedPlan
 from paper_2002_01935_b200.harness.workloads import load_workload
 from paper_2002_01935_b200.harness import generators as gen
-from paper_2002_01935_b200.harness.paths import best_greedy_tree
-from paper_2002_01935_b200.slicing import greedy_slice
-from paper_2002_01935_b200.tree import metrics
 
 tn, tree, ss, _ = load_workload("cfg4p_7x7_d20", ws=24)
 plan = SlicedPlan(tn, tree, ss, gemm_min_macs=2 ** 12, graph=False).bind()
