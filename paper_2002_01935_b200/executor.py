@@ -188,13 +188,23 @@ class SlicedPlan:
             for i, a in enumerate(arrays):
                 ptrs[i] = a.contiguous().data_ptr()
             return nat.LOC_DEVICE, dtype, ptrs, arrays
+        # re-binding the same (contiguous, right-dtype) host arrays -- new values in
+        # the same buffers, e.g. one bind per bitstring or per step -- reuses the
+        # marshalled pointer table; the library still copies the data every bind
+        cache = getattr(self, "_ptr_cache", None)
+        if (cache is not None and len(cache[0]) == len(arrays)
+                and all(a is b for a, b in zip(arrays, cache[0]))):
+            return nat.LOC_HOST, cache[1], cache[2], cache[3]
         conv = []
         dtype = nat.DTYPE_C64 if np.asarray(first).dtype == np.complex64 else nat.DTYPE_C128
         want = np.complex64 if dtype == nat.DTYPE_C64 else np.complex128
+        reusable = True
         for i, a in enumerate(arrays):
-            a = np.ascontiguousarray(a, dtype=want)
-            conv.append(a)
-            ptrs[i] = a.ctypes.data
+            c = np.ascontiguousarray(a, dtype=want)
+            reusable = reusable and c is a
+            conv.append(c)
+            ptrs[i] = c.__array_interface__["data"][0]
+        self._ptr_cache = (list(arrays), dtype, ptrs, conv) if reusable else None
         return nat.LOC_HOST, dtype, ptrs, conv
 
     @staticmethod
