@@ -345,6 +345,27 @@ cudaError_t launch_pack(const PackParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// block reduction of the fused perm-dot partial sums -> partial[blockIdx.x]
+__device__ __forceinline__ void perm_dot_reduce(float re, float im, float2* partial) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    re += __shfl_xor_sync(0xffffffffu, re, off);
+    im += __shfl_xor_sync(0xffffffffu, im, off);
+  }
+  __shared__ float2 red[8];
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = make_float2(re, im);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float2 v = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      v.x += red[w].x;
+      v.y += red[w].y;
+    }
+    partial[blockIdx.x] = v;
+  }
+}
+
 // ------------------------------------------------------------------ tiled permute
 __global__ void __launch_bounds__(256) perm_kernel(const PermParams p) {
   extern __shared__ __align__(16) unsigned char perm_smem[];
@@ -357,6 +378,7 @@ __global__ void __launch_bounds__(256) perm_kernel(const PermParams p) {
   float2* tile = reinterpret_cast<float2*>(perm_smem + ((size_t)(3 * ts * 4 + 15) & ~(size_t)15));
   for (int i = threadIdx.x; i < 3 * ts; i += blockDim.x) t_src[i] = p.tab[i];
   const int64_t nchunks = (p.n_outer + G - 1) / G;
+  float dre = 0.f, dim = 0.f;  // mode 5 partial sums
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
     const int64_t o0 = c * G;
     const int gcount = (int)(p.n_outer - o0 < (int64_t)G ? p.n_outer - o0 : (int64_t)G);
@@ -378,6 +400,14 @@ __global__ void __launch_bounds__(256) perm_kernel(const PermParams p) {
       const int j = e / ts, t = e - j * ts;
       const float2 v = tile[j * ts + t];
       const int64_t off = base_d[j] + t_dst[t];
+      if (p.mode == 5) {
+        const float2 xv = __ldg(p.dotx + off);
+        dre = fmaf(xv.x, v.x, dre);
+        dre = fmaf(-xv.y, v.y, dre);
+        dim = fmaf(xv.x, v.y, dim);
+        dim = fmaf(xv.y, v.x, dim);
+        continue;
+      }
       if (p.mode == 0) {
         static_cast<float2*>(p.dst)[off] = v;
       } else {
@@ -396,6 +426,7 @@ __global__ void __launch_bounds__(256) perm_kernel(const PermParams p) {
     }
     __syncthreads();
   }
+  if (p.mode == 5) perm_dot_reduce(dre, dim, p.partial);
 }
 
 // Vectorised variant: element pairs (t, t+1) are contiguous and 16 B / 8 B
@@ -450,6 +481,7 @@ __global__ void __launch_bounds__(256, 4) perm_vec_kernel(const PermParams p) {
   };
   int64_t c = blockIdx.x;
   if (c >= nchunks) return;
+  float dre = 0.f, dim = 0.f;  // mode 5 partial sums
   int buf = 0;
   bases(c, 0);
   __syncthreads();
@@ -478,6 +510,18 @@ __global__ void __launch_bounds__(256, 4) perm_vec_kernel(const PermParams p) {
       const int j = e >> half_lg, t = (e & half_mask) << 1;
       const float4 v = *reinterpret_cast<const float4*>(tile + perm_swz((j << lg) + t));
       const int64_t off = base_d[buf][j] + t_dst[t];
+      if (p.mode == 5) {  // fused dot: multiply with the other operand in place
+        const float4 xv = __ldg(reinterpret_cast<const float4*>(p.dotx + off));
+        dre = fmaf(xv.x, v.x, dre);
+        dre = fmaf(-xv.y, v.y, dre);
+        dim = fmaf(xv.x, v.y, dim);
+        dim = fmaf(xv.y, v.x, dim);
+        dre = fmaf(xv.z, v.z, dre);
+        dre = fmaf(-xv.w, v.w, dre);
+        dim = fmaf(xv.z, v.w, dim);
+        dim = fmaf(xv.w, v.z, dim);
+        continue;
+      }
       if (p.mode == 0) {
         __stcs(reinterpret_cast<float4*>(static_cast<float2*>(p.dst) + off), v);
       } else {
@@ -507,6 +551,7 @@ __global__ void __launch_bounds__(256, 4) perm_vec_kernel(const PermParams p) {
     c = cn;
     buf ^= 1;
   }
+  if (p.mode == 5) perm_dot_reduce(dre, dim, p.partial);
 }
 
 cudaError_t launch_perm(const PermParams& p, cudaStream_t st) {
@@ -524,6 +569,17 @@ cudaError_t launch_perm(const PermParams& p, cudaStream_t st) {
   }
   else
     perm_kernel<<<blocks, 256, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_perm_dot(PermParams p, float2* partial, float2* z, cudaStream_t st) {
+  p.mode = 5;
+  p.partial = partial;
+  const int64_t nchunks = (p.n_outer + p.group - 1) / p.group;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, 148 * 8));
+  cudaError_t e = launch_perm(p, st);
+  if (e != cudaSuccess) return e;
+  simt_finalize_kernel<<<1, 128, 0, st>>>(partial, z, 1, blocks);
   return cudaGetLastError();
 }
 

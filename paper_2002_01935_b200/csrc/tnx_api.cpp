@@ -607,7 +607,7 @@ int compile(Plan& P, const tnx_plan_desc* D) {
     }
     if (v.kind == VK_DOT) {
       if (x.labels != y.labels) v.blk_tmp = add_block(ph, 8 * y.size, st, st);
-      P.max_partial = std::max<int64_t>(P.max_partial, 148 * 4);
+      P.max_partial = std::max<int64_t>(P.max_partial, 148 * 8);  // dot / fused perm-dot block partials
     }
     if (v.kind == VK_GEMM) {
       const int64_t ra = v.swap ? v.N : v.M, rb = v.swap ? v.M : v.N;
@@ -898,9 +898,11 @@ int run_launches(Plan& P, const std::vector<Launch>& ls, cudaStream_t st, int st
       case L_PERM:
         e = launch_perm(P.perms[L.idx], st);
         break;
-      case L_DOT:
-        e = launch_dot(P.dots[L.idx], st);
+      case L_DOT: {
+        const DotParams& dp = P.dots[L.idx];
+        e = dp.perm >= 0 ? launch_perm_dot(P.perms[dp.perm], P.partial, dp.z, st) : launch_dot(dp, st);
         break;
+      }
       case L_RENORM: {
         const TensorLoc& t = P.T[L.idx];
         unsigned int* bits = P.d_absmax + L.idx;
@@ -1082,10 +1084,10 @@ int lower(Plan& P) {
             return fail(TNX_ERR_INVALID, "vertex " + std::to_string(v.ssa) + ": dot permute: " + err);
           pp.src = yp;
           pp.dst = tmp;
-          if (y.arena == AR_POOL && (y.offset & 1)) pp.vec = 0;
+          if ((y.arena == AR_POOL && (y.offset & 1)) || (x.arena == AR_POOL && (x.offset & 1))) pp.vec = 0;
           pp.tab = reinterpret_cast<const int32_t*>(toff);
+          pp.dotx = P.ptr(x);
           P.perms.push_back(pp);
-          out.push_back({L_PERM, (int)P.perms.size() - 1, v.ssa});
           yp = tmp;
         }
         DotParams dp{};
@@ -1095,6 +1097,9 @@ int lower(Plan& P) {
         dp.partial = P.partial;
         dp.n = x.size;
         dp.nblocks = 148 * 4;
+        // y in another layout: one fused launch reads y through the permute tile
+        // and multiplies with x in place (no permuted copy of y)
+        dp.perm = v.blk_tmp >= 0 ? (int)P.perms.size() - 1 : -1;
         P.dots.push_back(dp);
         out.push_back({L_DOT, (int)P.dots.size() - 1, v.ssa});
       } else {

@@ -75,11 +75,14 @@ struct PermParams {
   int64_t plane_stride;   // mode 1: elements per plane
   int32_t ts;
   int32_t group;
-  int32_t mode;           // 0: complex64 copy, 1: 4 split-TF32 planes,
-                          // 3 / 4: mixed TF32/BF16 planes for an A / B operand
+  int32_t mode;           // 0: complex64 copy, 1: 4 split-TF32 planes, 2: 6 planes (stacked B),
+                          // 3 / 4: mixed TF32/BF16 planes for an A / B operand,
+                          // 5: fused dot -- sum_i src_perm[i] * dotx[i] into per-block partials
   int32_t vec;            // 1: element pairs contiguous + aligned on both sides
   int32_t ts_log2;        // log2(ts) if ts is a power of two, else -1
   int32_t pad;
+  const float2* dotx;     // mode 5: the other operand, in the destination layout
+  float2* partial;        // mode 5: [gridDim.x] block partials
 };
 
 // Full contraction of two tensors in the same layout: z = sum_i x[i] y[i]
@@ -91,7 +94,7 @@ struct DotParams {
   float2* partial;
   int64_t n;
   int32_t nblocks;
-  int32_t pad;
+  int32_t perm;           // >= 0: y is read through this permute (fused perm-dot), else same layout
 };
 
 constexpr int kMaxLeafRank = 16;
@@ -167,6 +170,8 @@ cudaError_t launch_simt_batch(const SimtParams* jobs, const int32_t* block_start
 int simt_blocks(const SimtParams& p);
 cudaError_t launch_pack(const PackParams& p, cudaStream_t st);
 cudaError_t launch_perm(const PermParams& p, cudaStream_t st);
+// fused permute + dot (mode 5): z[0] = sum over the permuted src times dotx
+cudaError_t launch_perm_dot(PermParams p, float2* partial, float2* z, cudaStream_t st);
 cudaError_t launch_dot(const DotParams& p, cudaStream_t st);
 cudaError_t launch_accum(const AccumParams& p, cudaStream_t st);
 cudaError_t launch_allreduce(const double2* acc, const double2* comp, const long long* exps, int n,
