@@ -390,6 +390,15 @@ def main():
     hbm = {"kernels": "perm_vec/perm/pack/dot", "achieved_gbs": mem_bytes / (mem_ms / 1e3) / 1e9 if mem_ms else None,
            "peak_gbs": peaks["hbm_gbs"], "frac": (mem_bytes / (mem_ms / 1e3) / 1e9 / peaks["hbm_gbs"]) if mem_ms else None,
            "ms_per_slice": mem_ms}
+    # the aggregate is dominated by many sub-MB launches (latency-bound); the large
+    # launches show the kernels' bandwidth
+    big = [(t, b) for k, v, t, b in prof_b if (k == "pack" or (k == "simt" and b > 0)) and b >= 16e6]
+    if big:
+        bt, bb = sum(t for t, _ in big), sum(b for _, b in big)
+        hbm["large_launches"] = {"min_bytes": 16e6, "count": len(big), "achieved_gbs": bb / (bt / 1e3) / 1e9,
+                                 "frac": bb / (bt / 1e3) / 1e9 / peaks["hbm_gbs"]}
+    small = [b for k, v, t, b in prof_b if (k == "pack" or (k == "simt" and b > 0)) and b < 16e6]
+    hbm["small_launches"] = {"count": len(small), "median_bytes": float(np.median(small)) if small else None}
     by_kind = {}
     for k, v, t in prof:
         by_kind[k] = by_kind.get(k, 0.0) + t
