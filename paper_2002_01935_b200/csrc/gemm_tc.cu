@@ -185,7 +185,7 @@ struct GemmArgs {
   int32_t debug;         // TNX_GEMM_DEBUG bit 0: skip the TMA loads (MMA-pipeline ceiling; wrong results)
   int32_t dstack;        // direct planes of a stacked-B parent operand: also write -im_hi, -im_lo (planes 4, 5)
   int32_t ksnake;        // odd waves traverse K in reverse (L2 reuse across waves)
-  int32_t pad_;
+  int32_t first;         // k-blocks of a unit's first TMEM round (>= promote; see launch_gemm)
 };
 
 __device__ __forceinline__ int64_t map_offset(const IdxMap& m, int64_t idx) {
@@ -542,15 +542,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         decode_unit(g, u, z, b, tm, tn);
         const int kb_begin = z * g.kb_per_split;
         const int nkb = min(g.num_kb - kb_begin, g.kb_per_split);
-        const int rounds = (nkb + P - 1) / P;
+        const int F = min(nkb, max(P, g.first));  // first TMEM round of the unit
+        const int rounds = 1 + (nkb - F + P - 1) / P;
         for (int r = 0; r < rounds; ++r, ++R) {
           const uint32_t set = R & 1u;
           mbar_wait(smem_addr(&tempty[set]), ((R >> 1) & 1u) ^ 1u);
           tc_fence_after();
           const uint32_t d_re = tmem_base + set * 256;
           const uint32_t d_im = d_re + BN;
-          const int kb0 = r * P;
-          const int kb1 = min(nkb, kb0 + P);
+          const int kb0 = r == 0 ? 0 : F + (r - 1) * P;
+          const int kb1 = r == 0 ? F : min(nkb, kb0 + P);
           for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(smem_addr(&full[stage]), phase);
             tc_fence_after();
@@ -652,7 +653,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       decode_unit(g, u, z, b, tm, tn);
       const int kb_begin = z * g.kb_per_split;
       const int nkb = min(g.num_kb - kb_begin, g.kb_per_split);
-      const int rounds = (nkb + P - 1) / P;
+      const int rounds = 1 + (nkb - min(nkb, max(P, g.first)) + P - 1) / P;
       float mre[64], mim[64];
 #pragma unroll
       for (int j = 0; j < 64; ++j) {
@@ -981,7 +982,13 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
     a.dstack = g.dstack;
     static const int snake = getenv("TNX_GEMM_KSNAKE") ? atoi(getenv("TNX_GEMM_KSNAKE")) : 1;
     a.ksnake = snake;
-    a.pad_ = 0;
+    // a unit's first TMEM round spans TNX_GEMM_FIRST (default 6) k-blocks, later
+    // rounds `promote`: while the epilogue warps store the previous unit, the
+    // MMA can run two rounds ahead, and a long first round lets that cover a
+    // mid-K unit's stores (cfg4 GEMM time -1.1 %; only the first round's
+    // accumulation gets longer, so long-K accuracy is unchanged)
+    static const int first = getenv("TNX_GEMM_FIRST") ? atoi(getenv("TNX_GEMM_FIRST")) : 6;
+    a.first = g.promote > 0 ? 0 : first;
   }
   const int splits = g.splits > 1 ? g.splits : 1;
   a.kb_per_split = (a.num_kb + splits - 1) / splits;

@@ -543,5 +543,7 @@ def test_stacked_parent_fed_by_direct_children():
         vals.append(plan.result())
         plan.close()
     ref, _, _ = oracle.contract(tn, tree)
+    # two chained GEMMs; the parent's 8-k-block units run a 6-k-block first TMEM
+    # round (TNX_GEMM_FIRST), so allow ~2e-6 per GEMM (north star: 1e-5)
     for v in vals:
-        assert rel_err(v, ref) <= 2e-6
+        assert rel_err(v, ref) <= 5e-6
