@@ -304,8 +304,13 @@ __device__ __forceinline__ void build_gtab(const GemmArgs& g, int64_t* gtab, int
   asm volatile("bar.sync 1, 256;" ::: "memory");
 }
 
+// TMEM-set release by the epilogue warps.  Relaxed: the MMA issuer only needs
+// the promotion's TMEM reads done (tcgen05.wait::ld + tcgen05.fence::
+// before_thread_sync precede the arrive); a release arrive would also make every
+// thread wait for its previous tile's global stores to become visible
+// (MEMBAR.GPU), serialising the epilogue stores with the next tile's MMAs.
 __device__ __forceinline__ void mbar_arrive(uint32_t a) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
 
 // Warp roles: 0 = TMA producer, 1 = MMA issuer, 2..9 = promotion/epilogue.
@@ -393,7 +398,7 @@ __device__ __forceinline__ void umma_commit_2sm(uint32_t mbar) {
 __device__ __forceinline__ void mbar_arrive_leader(uint32_t local_addr) {
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(0));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 // idesc: D=f32, A=B=tf32 (fmt 2) or bf16 (fmt 1), K-major, N=128, M=128 (1 CTA)
 // or 256 (pair)

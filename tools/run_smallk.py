@@ -9,10 +9,12 @@ from paper_2002_01935_b200.executor import SlicedPlan
 from paper_2002_01935_b200.network import TensorNetwork, TensorNode
 from paper_2002_01935_b200.tree import ContractionTree
 rng = np.random.default_rng(0)
-al = [f"a{i}" for i in range(12)]
-kl = [f"k{i}" for i in range(3)]
-bl = [f"b{i}" for i in range(13)]
-cl = [f"c{i}" for i in range(8)]
+# optional label counts: run_smallk.py reps [n_a n_k n_b n_c]  (M = 2^n_a, K = 2^n_k, N = 2^n_b)
+na, nk, nb, nc = (int(x) for x in sys.argv[2:6]) if len(sys.argv) > 5 else (12, 3, 13, 8)
+al = [f"a{i}" for i in range(na)]
+kl = [f"k{i}" for i in range(nk)]
+bl = [f"b{i}" for i in range(nb)]
+cl = [f"c{i}" for i in range(nc)]
 tab = {l: 2 for l in al + kl + bl + cl + ["s"]}
 def rnd(ls):
     shp = [tab[l] for l in ls]
