@@ -83,7 +83,12 @@ def gemm():
     wr = scaled(d, units, "dram__bytes_write.sum")
     M = N = 8192
     K = 4096
-    alg = 16 * (M * K + K * N) + 8 * M * N  # 4 fp32 planes of A and B + c64 output
+    # operand planes read once + c64 output: A 4 fp32 planes; B 4, or 6 for the
+    # stacked-B instance (template argument 4 = 1: -im_hi, -im_lo planes)
+    name = d["Kernel Name"]
+    targs = name[name.find("<") + 1:name.find(">")].split(",") if "<" in name else []
+    stacked = len(targs) >= 4 and targs[3].strip() in ("1", "true")
+    alg = 16 * M * K + (24 if stacked else 16) * K * N + 8 * M * N
     flops = 8 * M * N * K
     out = {"kernel": d["Kernel Name"],
            "command": "ncu --set full --clock-control none --import-source on -k regex:gemm_c64 -c 1 "
