@@ -86,7 +86,8 @@ def gemm():
     # operand planes read once + c64 output: A 4 fp32 planes; B 4, or 6 for the
     # stacked-B instance (template argument 4 = 1: -im_hi, -im_lo planes)
     name = d["Kernel Name"]
-    targs = name[name.find("<") + 1:name.find(">")].split(",") if "<" in name else []
+    i0 = name.find("kernel<")
+    targs = name[i0 + 7:name.find(">", i0)].split(",") if i0 >= 0 else []
     stacked = len(targs) >= 4 and targs[3].strip() in ("1", "true")
     alg = 16 * M * K + (24 if stacked else 16) * K * N + 8 * M * N
     flops = 8 * M * N * K
