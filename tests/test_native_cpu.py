@@ -146,3 +146,52 @@ def test_allreduce_argument_checks():
     finally:
         a.close()
         b.close()
+
+
+def _raw_desc(dims, leaves, pairs, out=(), sliced=()):
+    """Plan descriptor straight through the C ABI (no Python wrapper checks)."""
+    import ctypes as C
+    flat = [l for lv in leaves for l in lv]
+    keep = []  # keep the ctypes arrays alive with the struct
+
+    def arr(t, xs):
+        a = (t * max(1, len(xs)))(*xs)
+        keep.append(a)
+        return a
+    d = nat.PlanDesc(len(dims), arr(C.c_int64, dims), len(leaves), arr(C.c_int32, [len(l) for l in leaves]),
+                     arr(C.c_int32, flat), arr(C.c_int32, [c for p in pairs for c in p]),
+                     len(out), arr(C.c_int32, out), len(sliced), arr(C.c_int32, sliced),
+                     nat.PREC_3XTF32, 0, 0, 0, 0.0)
+    return d, keep
+
+
+def test_c_abi_status_codes():
+    """tnx_plan_create / run / result error paths: invalid descriptors give
+    TNX_ERR_INVALID with a message, calls out of order give TNX_ERR_STATE;
+    nothing touches a GPU."""
+    import ctypes as C
+    lib = nat.load()
+    h = C.c_void_p()
+    # matrix chain a-b-c: x[a,b] y[b,c] z[c,a] -> scalar
+    good_leaves = [[0, 1], [1, 2], [2, 0]]
+    d, keep = _raw_desc([2, 3, 4], good_leaves, [(0, 1), (3, 2)])
+    assert lib.tnx_plan_create(C.byref(d), C.byref(h)) == nat.TNX_OK
+    assert lib.tnx_run_slices(h, 0, 1, None) == nat.TNX_ERR_STATE
+    assert b"bind" in lib.tnx_last_error()
+    out = (C.c_double * 2)()
+    assert lib.tnx_partial_result(h, out, 1, None) == nat.TNX_ERR_STATE
+    assert lib.tnx_plan_destroy(h) == nat.TNX_OK
+    bad = [
+        _raw_desc([2, 3, 4], good_leaves, [(0, 1), (0, 2)]),          # leaf consumed twice
+        _raw_desc([2, 3, 4], good_leaves, [(0, 1), (4, 2)]),          # vertex not yet built
+        _raw_desc([2, 3, 4], [[0, 1], [1, 7], [2, 0]], [(0, 1), (3, 2)]),  # label id out of range
+        _raw_desc([2, 3, 4], good_leaves, [(0, 1), (3, 2)], out=(0,), sliced=(0,)),  # sliced output
+        _raw_desc([2, 0, 4], good_leaves, [(0, 1), (3, 2)]),          # zero dimension
+    ]
+    for d, keep in bad:
+        h = C.c_void_p()
+        rc = lib.tnx_plan_create(C.byref(d), C.byref(h))
+        assert rc in (nat.TNX_ERR_INVALID, nat.TNX_ERR_DATA), rc
+        assert lib.tnx_last_error(), "error message expected"
+        assert not h.value
+    assert lib.tnx_plan_create(None, C.byref(h)) == nat.TNX_ERR_INVALID
