@@ -474,6 +474,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_before();
   if constexpr (TWO_SM) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
+  // prologue above (TMEM allocation, barrier init) overlaps the predecessor's
+  // tail under programmatic dependent launch; its outputs are read only below
+  pdl_wait();
   const uint32_t tmem_base = *tmem_slot;
   const int P = g.promote;
 
@@ -921,6 +924,7 @@ int gemm_prepare(GemmPlan* g, const float* a_planes, const float* b_planes, floa
 
 __global__ void splitk_reduce_kernel(const float4* __restrict__ part, float4* __restrict__ out,
                                      int64_t n4, int64_t stride4, int splits) {
+  pdl_wait();
   const int64_t step = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += step) {
     float4 a = part[i];
@@ -1022,22 +1026,29 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(NUM_THREADS);
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
+  int nattr = 0;
+  if (pdl_enabled()) {
+    attr[nattr].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[nattr].val.programmaticStreamSerializationAllowed = 1;
+    ++nattr;
+  }
+  cfg.attrs = attr;
   if (g.two_sm) {
     const int64_t clusters = std::min<int64_t>(units, 74);
     cfg.gridDim = dim3((unsigned)(2 * clusters));
     cfg.dynamicSmemBytes = g.stackb ? KCfg<true, true>::SMEM : KCfg<true>::SMEM;
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    attr[nattr].id = cudaLaunchAttributeClusterDimension;
+    attr[nattr].val.clusterDim.x = 2;
+    attr[nattr].val.clusterDim.y = 1;
+    attr[nattr].val.clusterDim.z = 1;
+    cfg.numAttrs = nattr + 1;
     cudaError_t le = cudaLaunchKernelEx(&cfg, gemm_kernel_for<true>(a.mix != 0, epi, g.stackb != 0), *ta, *tb, a);
     if (le != cudaSuccess) return le;
   } else {
     cfg.gridDim = dim3((unsigned)std::min<int64_t>(units, 148));
     cfg.dynamicSmemBytes = KCfg<false>::SMEM;
+    cfg.numAttrs = nattr;
     cudaError_t le = cudaLaunchKernelEx(&cfg, gemm_kernel_for<false>(a.mix != 0, epi), *ta, *tb, a);
     if (le != cudaSuccess) return le;
   }
@@ -1047,7 +1058,7 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
   if (n % 2 != 0) return cudaErrorInvalidValue;
   const int64_t n4 = n / 2;
   int blocks = (int)std::min<int64_t>((n4 + 255) / 256, 148 * 16);
-  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(g.partial),
+  launch_pdl(splitk_reduce_kernel, blocks, 256, 0, st, reinterpret_cast<const float4*>(g.partial),
                                                reinterpret_cast<float4*>(g.out), n4, n4, zs);
   return cudaGetLastError();
 }

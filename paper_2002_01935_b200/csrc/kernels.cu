@@ -13,6 +13,7 @@
 //  K6 accum   : root -> tn.output order, Kahan-compensated complex128
 //               accumulation across slices.
 #include <climits>
+#include <cstdlib>
 #include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -69,6 +70,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherJob* __restrict
                                                      const int32_t* __restrict__ start, int njobs,
                                                      const float2* __restrict__ pool,
                                                      const unsigned long long* __restrict__ counter) {
+  pdl_wait();
   int lo = 0, hi = njobs - 1;
   const int b = blockIdx.x;
   while (lo < hi) {
@@ -119,7 +121,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherJob* __restrict
 cudaError_t launch_gather(const GatherJob* jobs, const int32_t* start, int njobs, int total_blocks,
                           const float2* pool, const unsigned long long* counter, cudaStream_t st) {
   if (njobs == 0) return cudaSuccess;
-  gather_kernel<<<total_blocks, 256, 0, st>>>(jobs, start, njobs, pool, counter);
+  launch_pdl(gather_kernel, total_blocks, 256, 0, st, jobs, start, njobs, pool, counter);
   return cudaGetLastError();
 }
 
@@ -168,6 +170,7 @@ __device__ __forceinline__ void simt_sum(const SimtParams& p, int64_t ox, int64_
 }
 
 __global__ void __launch_bounds__(256) simt_split_kernel(const SimtParams p) {
+  pdl_wait();
   // grid: (nsplit, out_size)
   const int64_t o = blockIdx.y;
   const int64_t j0 = (int64_t)blockIdx.x * p.chunk;
@@ -198,6 +201,7 @@ __global__ void __launch_bounds__(256) simt_split_kernel(const SimtParams p) {
 
 __global__ void simt_finalize_kernel(const float2* __restrict__ partial, float2* __restrict__ z,
                                      int64_t out_size, int nsplit) {
+  pdl_wait();
   const int64_t o = blockIdx.x;
   double re = 0.0, im = 0.0;
   for (int i = threadIdx.x; i < nsplit; i += blockDim.x) {
@@ -239,10 +243,10 @@ cudaError_t launch_simt(const SimtParams& p, cudaStream_t st) {
   if (p.mode != SIMT_SPLIT) return cudaErrorInvalidValue;
   {
     dim3 grid((unsigned)p.nsplit, (unsigned)p.out_size);
-    simt_split_kernel<<<grid, 256, 0, st>>>(p);
+    launch_pdl(simt_split_kernel, grid, 256, 0, st, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    simt_finalize_kernel<<<(unsigned)p.out_size, 128, 0, st>>>(p.partial, p.z, p.out_size, p.nsplit);
+    launch_pdl(simt_finalize_kernel, (unsigned)p.out_size, 128, 0, st, p.partial, p.z, p.out_size, p.nsplit);
   }
   return cudaGetLastError();
 }
@@ -250,6 +254,7 @@ cudaError_t launch_simt(const SimtParams& p, cudaStream_t st) {
 // ------------------------------------------------------------------ batched simt
 __global__ void __launch_bounds__(256) simt_batch_kernel(const SimtParams* __restrict__ jobs,
                                                          const int32_t* __restrict__ start, int njobs) {
+  pdl_wait();
   // locate this block's job (binary search over the block prefix)
   int lo = 0, hi = njobs - 1;
   const int b = blockIdx.x;
@@ -298,12 +303,13 @@ int simt_blocks(const SimtParams& p) {
 cudaError_t launch_simt_batch(const SimtParams* jobs, const int32_t* block_start, int njobs,
                               int total_blocks, cudaStream_t st) {
   if (njobs == 0) return cudaSuccess;
-  simt_batch_kernel<<<total_blocks, 256, 0, st>>>(jobs, block_start, njobs);
+  launch_pdl(simt_batch_kernel, total_blocks, 256, 0, st, jobs, block_start, njobs);
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ pack
 __global__ void __launch_bounds__(256) pack_kernel(const PackParams p) {
+  pdl_wait();
   // destination planes are K-blocked: offset(r, k) = ((k / 16) * rows + r) * 16 + k % 16
   const int64_t total = p.rows * p.kp;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -341,7 +347,7 @@ __global__ void __launch_bounds__(256) pack_kernel(const PackParams p) {
 }
 
 cudaError_t launch_pack(const PackParams& p, cudaStream_t st) {
-  pack_kernel<<<grid_for(p.rows * p.kp, 256, 148 * 32), 256, 0, st>>>(p);
+  launch_pdl(pack_kernel, grid_for(p.rows * p.kp, 256, 148 * 32), 256, 0, st, p);
   return cudaGetLastError();
 }
 
@@ -368,6 +374,7 @@ __device__ __forceinline__ void perm_dot_reduce(float re, float im, float2* part
 
 // ------------------------------------------------------------------ tiled permute
 __global__ void __launch_bounds__(256) perm_kernel(const PermParams p) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char perm_smem[];
   __shared__ int64_t base_s[64], base_d[64];
   const int ts = p.ts;
@@ -442,6 +449,7 @@ __device__ __forceinline__ int perm_swz(int i) {
 constexpr int kPermMaxPairs = 4;  // (ts * group / 2) / 256 <= 2048 / 2 / 256 (vec needs ts <= 2048)
 
 __global__ void __launch_bounds__(256, 4) perm_vec_kernel(const PermParams p) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char perm_smem[];
   __shared__ int64_t base_s[2][64], base_d[2][64];
   const int ts = p.ts;
@@ -565,10 +573,10 @@ cudaError_t launch_perm(const PermParams& p, cudaStream_t st) {
       return true;
     }();
     (void)carveout;
-    perm_vec_kernel<<<blocks, 256, smem, st>>>(p);
+    launch_pdl(perm_vec_kernel, blocks, 256, smem, st, p);
   }
   else
-    perm_kernel<<<blocks, 256, smem, st>>>(p);
+    launch_pdl(perm_kernel, blocks, 256, smem, st, p);
   return cudaGetLastError();
 }
 
@@ -579,12 +587,13 @@ cudaError_t launch_perm_dot(PermParams p, float2* partial, float2* z, cudaStream
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, 148 * 8));
   cudaError_t e = launch_perm(p, st);
   if (e != cudaSuccess) return e;
-  simt_finalize_kernel<<<1, 128, 0, st>>>(partial, z, 1, blocks);
+  launch_pdl(simt_finalize_kernel, 1, 128, 0, st, partial, z, 1, blocks);
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ dot
 __global__ void __launch_bounds__(256) dot_kernel(const DotParams p) {
+  pdl_wait();
   const int64_t n2 = p.n >> 1;  // complex pairs (16 B)
   const float4* x4 = reinterpret_cast<const float4*>(p.x);
   const float4* y4 = reinterpret_cast<const float4*>(p.y);
@@ -625,15 +634,16 @@ __global__ void __launch_bounds__(256) dot_kernel(const DotParams p) {
 }
 
 cudaError_t launch_dot(const DotParams& p, cudaStream_t st) {
-  dot_kernel<<<p.nblocks, 256, 0, st>>>(p);
+  launch_pdl(dot_kernel, p.nblocks, 256, 0, st, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  simt_finalize_kernel<<<1, 128, 0, st>>>(p.partial, p.z, 1, p.nblocks);
+  launch_pdl(simt_finalize_kernel, 1, 128, 0, st, p.partial, p.z, 1, p.nblocks);
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ accumulate
 __global__ void accum_kernel(const AccumParams p) {
+  pdl_wait();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (int64_t o = tid; o < p.out_size; o += stride) {
@@ -682,7 +692,7 @@ __global__ void accum_kernel(const AccumParams p) {
 }
 
 cudaError_t launch_accum(const AccumParams& p, cudaStream_t st) {
-  accum_kernel<<<grid_for(p.out_size, 256, 148 * 8), 256, 0, st>>>(p);
+  launch_pdl(accum_kernel, grid_for(p.out_size, 256, 148 * 8), 256, 0, st, p);
   return cudaGetLastError();
 }
 
@@ -692,6 +702,7 @@ cudaError_t launch_accum(const AccumParams& p, cudaStream_t st) {
 __global__ void allreduce_kernel(const double2* __restrict__ acc, const double2* __restrict__ comp,
                                  const long long* __restrict__ exps, int n, int64_t out_size,
                                  double2* out_acc, double2* out_comp, long long* out_exp) {
+  pdl_wait();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < out_size; o += stride) {
     if (exps) {
@@ -733,12 +744,13 @@ __global__ void allreduce_kernel(const double2* __restrict__ acc, const double2*
 cudaError_t launch_allreduce(const double2* acc, const double2* comp, const long long* exps, int n,
                              int64_t out_size, double2* out_acc, double2* out_comp, long long* out_exp,
                              cudaStream_t st) {
-  allreduce_kernel<<<grid_for(out_size, 256, 148 * 8), 256, 0, st>>>(acc, comp, exps, n, out_size, out_acc,
+  launch_pdl(allreduce_kernel, grid_for(out_size, 256, 148 * 8), 256, 0, st, acc, comp, exps, n, out_size, out_acc,
                                                                     out_comp, out_exp);
   return cudaGetLastError();
 }
 
 __global__ void absmax_kernel(const float2* __restrict__ z, int64_t n, unsigned int* bits) {
+  pdl_wait();
   float m = 0.f;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -752,6 +764,7 @@ __global__ void absmax_kernel(const float2* __restrict__ z, int64_t n, unsigned 
 
 __global__ void rescale_kernel(float2* __restrict__ z, int64_t n, const unsigned int* bits,
                                long long* exp_acc) {
+  pdl_wait();
   const float m = __uint_as_float(*bits);
   if (!(m > 0.f) || !isfinite(m)) return;
   int e;
@@ -766,24 +779,26 @@ __global__ void rescale_kernel(float2* __restrict__ z, int64_t n, const unsigned
 }
 
 cudaError_t launch_absmax(const float2* z, int64_t n, unsigned int* bits, cudaStream_t st) {
-  absmax_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(z, n, bits);
+  launch_pdl(absmax_kernel, grid_for(n, 256, 148 * 8), 256, 0, st, z, n, bits);
   return cudaGetLastError();
 }
 
 cudaError_t launch_rescale(float2* z, int64_t n, const unsigned int* bits, long long* exp_acc,
                            cudaStream_t st) {
-  rescale_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(z, n, bits, exp_acc);
+  launch_pdl(rescale_kernel, grid_for(n, 256, 148 * 8), 256, 0, st, z, n, bits, exp_acc);
   return cudaGetLastError();
 }
 
-__global__ void set_counter_kernel(unsigned long long* c, unsigned long long v) { *c = v; }
+__global__ void set_counter_kernel(unsigned long long* c, unsigned long long v) {
+  pdl_wait(); *c = v; }
 
 cudaError_t launch_set_counter(unsigned long long* counter, unsigned long long v, cudaStream_t st) {
-  set_counter_kernel<<<1, 1, 0, st>>>(counter, v);
+  launch_pdl(set_counter_kernel, 1, 1, 0, st, counter, v);
   return cudaGetLastError();
 }
 
 __global__ void convert_kernel(const double2* __restrict__ s, float2* __restrict__ d, int64_t n) {
+  pdl_wait();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
     d[i] = make_float2((float)s[i].x, (float)s[i].y);
@@ -791,7 +806,7 @@ __global__ void convert_kernel(const double2* __restrict__ s, float2* __restrict
 
 cudaError_t launch_convert_c128(const double2* src, float2* dst, int64_t n, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
-  convert_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(src, dst, n);
+  launch_pdl(convert_kernel, grid_for(n, 256, 148 * 8), 256, 0, st, src, dst, n);
   return cudaGetLastError();
 }
 

@@ -3,7 +3,35 @@
 // parameters; all offsets are in elements.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
+#ifdef __CUDACC__
+// Programmatic dependent launch: every kernel is launched with programmatic
+// stream serialisation so its launch and prologue overlap the predecessor's
+// tail, and waits (griddepcontrol.wait) before reading anything a predecessor
+// wrote.  TNX_PDL=0 launches plainly (the wait is then a no-op).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+inline int pdl_enabled() {
+  static const int v = getenv("TNX_PDL") ? atoi(getenv("TNX_PDL")) : 1;
+  return v;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+#endif
+
 #ifdef __CUDACC__
 #include <cuda_bf16.h>
 #endif
