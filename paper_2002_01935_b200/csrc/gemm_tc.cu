@@ -4,19 +4,30 @@
 //
 //   C[b,m,n] = sum_k A[b,m,k] * B[b,n,k]          (complex64 in/out)
 //
-// Operands arrive as four fp32 planes each ([re_hi, re_lo, im_hi, im_lo]),
-// K-blocked [plane][kp/16][batch*rows][16] so that every TMA box (3-D tensor
-// map) is one contiguous 8 KB block, written by the pack kernels.  Per 8-wide k-step
-// one elected thread issues 12 tcgen05.mma.kind::tf32 (M=128, N=128, K=8):
-//
 //   Cre += Ar_h Br_h + Ar_h Br_l + Ar_l Br_h - (Ai_h Bi_h + Ai_h Bi_l + Ai_l Bi_h)
 //   Cim += Ar_h Bi_h + Ar_h Bi_l + Ar_l Bi_h +  Ai_h Br_h + Ai_h Br_l + Ai_l Br_h
 //
-// (the minus uses the instruction descriptor's negate-A bit), accumulating
-// in FP32 TMEM accumulators.  A warp-specialised mbarrier pipeline (TMA
-// producer / MMA issuer) streams 3 stages of 64 KB; every `promote` k-blocks
-// the partial accumulators are promoted into FP32 registers of 8 epilogue
-// warps (TMEM double-buffered), which finally store interleaved complex64.
+// Operands are fp32 planes [re_hi, re_lo, im_hi, im_lo] (+ [-im_hi, -im_lo]
+// for a stacked-B operand), K-blocked [plane][kp/16][batch*rows][16] so every
+// TMA box (3-D tensor map) is one contiguous block; written by the pack /
+// permute kernels or directly by a child GEMM's epilogue.
+//
+// One persistent kernel template, instantiated per (2-CTA pair, precision,
+// epilogue mode, stacked B): warp 0 lane 0 = TMA producer (smem ring), warp 1
+// lane 0 = MMA issuer, warps 2-9 = promotion + epilogue.
+//   * 1-CTA: 128x128 tiles, 12 tcgen05.mma (N=128) per 8-wide k-step.
+//   * 2-CTA (cta_group::2): 256x128 pair tiles, each CTA stages its 128 A rows
+//     and half of B.  Stacked B: each CTA stages full 128-row B slots
+//     ([re|-im] / [im|re]) and 6 N=256 MMAs per k-step accumulate straight into
+//     the [Re | Im] TMEM columns (shared-memory operand traffic -17 %).
+//   * Tensor-core accumulation rounds toward zero, so every `promote` k-blocks
+//     (the first round of a unit: `first`) the TMEM accumulator set (two sets,
+//     double-buffered) is added into FP32 registers of the epilogue warps,
+//     which release it with a relaxed mbarrier arrive.
+//   * Epilogue: interleaved complex64, split-K partials, or the parent GEMM's
+//     operand planes (GEMM->GEMM fusion).
+//   * Launch: cost model over (2-CTA, split-K), grid = min(units, SMs / pairs),
+//     programmatic dependent launch (griddepcontrol.wait after the prologue).
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -33,10 +44,6 @@ namespace {
 constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int BK = 16;                          // fp32 per smem row (64 B, SWIZZLE_64B)
-constexpr int STAGES = 3;
-constexpr int PLANE_BYTES = BM * BK * 4;        // 8 KB per plane tile
-constexpr int STAGE_BYTES = 8 * PLANE_BYTES;    // 4 A planes + 4 B planes
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 constexpr int TMEM_COLS = 512;
 constexpr int GROUP_M = 8;
 
