@@ -1,17 +1,23 @@
-// SIMT kernels of the sliced contraction executor (sm_100a).
+// Memory-bound kernels of the sliced contraction executor (sm_100a).  Every
+// kernel starts with griddepcontrol.wait (programmatic dependent launch).
 //
 //  K1 gather  : fix_index of every slice-dependent leaf for the current slice
 //               id (reference dense.py:161-170), read from a device counter so
-//               the per-slice CUDA graph needs no host update.
-//  K4 simt    : generic strided pairwise contraction (reference
-//               pairwise_contract, dense.py:61-76) in FP32 complex:
-//               thread-per-output, warp-per-output (lane-split sum, shuffle
-//               reduce) and split-reduction (block partials + finalize) modes.
-//  K2 pack    : permute a complex64 tensor into the four split-TF32 planes the
-//               tcgen05 GEMM consumes, K-blocked [kp/16][rows][16] (gather
-//               fallback; the tiled permute `perm_kernel` is the fast path).
+//               the per-slice CUDA graph needs no host update; one launch, block
+//               ranges per leaf, contiguous runs merged, 16 B copies.
+//  K4 simt    : strided pairwise contraction (reference pairwise_contract,
+//               dense.py:61-76) in FP32 complex: all thread/warp-mode vertices
+//               of a dependency level in one batched launch (2^lg lanes per
+//               output), split mode (block partials + FP64 finalize) for long
+//               sums; strided fast path with 16 B loads.
+//  K2 pack / permute : complex64 -> split-TF32 planes the tcgen05 GEMM consumes,
+//               K-blocked [kp/16][rows][16]; shared-memory tiled, pipelined
+//               permute (`perm_vec_kernel`), gather fallback (`pack_kernel`);
+//               mode 5 fuses a full contraction (permute + dot).
+//  K5 dot     : streaming complex dot for equal layouts.
 //  K6 accum   : root -> tn.output order, Kahan-compensated complex128
-//               accumulation across slices.
+//               accumulation across slices; allreduce_kernel sums
+//               several plans' accumulators (tnx_allreduce).
 #include <climits>
 #include <cstdlib>
 #include <algorithm>
