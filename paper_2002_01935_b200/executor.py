@@ -424,11 +424,24 @@ def contract(tn, tree, options=None, **kw):
     return contract_sliced(tn, tree, (), options, **kw)
 
 
+_OPEN = ("x", "X", "*")
+
+
 def _project(tn, bitstring):
-    """Fix the open legs (tn.output order) to the bitstring (column projection)."""
+    """Fix the open legs (tn.output order) to the bitstring (column projection,
+    SPEC.md:533-537).  Positions marked 'x' / '*' stay open: they become the
+    projected network's output legs, in qubit order, so the contraction yields
+    the 2^N_f amplitudes of the open qubits at once (PAPER.md N_f open qubits)."""
     if len(bitstring) != len(tn.output):
         raise ValueError(f"bitstring length {len(bitstring)} != {len(tn.output)} open legs")
-    fix = {lbl: int(b) for lbl, b in zip(tn.output, bitstring)}
+    fix, keep = {}, []
+    for lbl, b in zip(tn.output, bitstring):
+        if b in _OPEN:
+            keep.append(lbl)
+            continue
+        if not str(b).isdigit():
+            raise ValueError(f"bitstring character {b!r} is neither a digit nor an open marker")
+        fix[lbl] = int(b)
     nodes = []
     for nd in tn.nodes:
         data, labels = nd.data, list(nd.indices)
@@ -443,20 +456,34 @@ def _project(tn, bitstring):
                 labels.pop(ax)
         nodes.append(TensorNode(nd.id, labels, data))
     table = {l: d for l, d in tn.index_table.items() if l not in fix}
-    return TensorNetwork(nodes, table, (), tn.norm_exponent)
+    return TensorNetwork(nodes, table, tuple(keep), tn.norm_exponent)
+
+
+def _open_pattern(bitstring):
+    return tuple(i for i, b in enumerate(bitstring) if b in _OPEN)
 
 
 class AmplitudeEngine:
     """One compiled plan reused across bitstrings (only leaf data changes,
-    PAPER.md:530; SPEC.md:533-537)."""
+    PAPER.md:530).  ``open_qubits`` (positions, or a pattern
+    string with 'x' marks) selects legs left open: every call must then mark
+    exactly those positions and returns the (2,)*N_f amplitude tensor."""
 
-    def __init__(self, circuit_tn, tree, slice_set=(), device=0, precision=None):
+    def __init__(self, circuit_tn, tree, slice_set=(), device=0, precision=None, open_qubits=()):
         self.tn = circuit_tn
         self.tree = tree
-        base = _project(circuit_tn, "0" * len(circuit_tn.output))
-        self.plan = SlicedPlan(base, tree, slice_set, device=device, precision=precision)
+        if isinstance(open_qubits, str):
+            open_qubits = _open_pattern(open_qubits)
+        self.open = tuple(sorted(int(i) for i in open_qubits))
+        n = len(circuit_tn.output)
+        if any(not 0 <= i < n for i in self.open):
+            raise ValueError(f"open qubit positions {self.open} out of range for {n} legs")
+        base = "".join("x" if i in self.open else "0" for i in range(n))
+        self.plan = SlicedPlan(_project(circuit_tn, base), tree, slice_set, device=device, precision=precision)
 
     def __call__(self, bitstring):
+        if _open_pattern(bitstring) != self.open:
+            raise ValueError(f"open positions of {bitstring!r} differ from the engine's {self.open}")
         ptn = _project(self.tn, bitstring)
         self.plan.bind(ptn)
         self.plan.run()
@@ -468,8 +495,10 @@ class AmplitudeEngine:
 
 
 def amplitude(circuit_tn, bitstring, tree, slice_set=(), **kw):
-    """c_x = <x| U |0> of a circuit network whose open legs are the qubits."""
-    eng = AmplitudeEngine(circuit_tn, tree, slice_set, **kw)
+    """c_x = <x| U |0> of a circuit network whose open legs are the qubits
+    (SPEC.md:533); 'x' / '*' in the bitstring leave that qubit open and return
+    the amplitude tensor over the open qubits."""
+    eng = AmplitudeEngine(circuit_tn, tree, slice_set, open_qubits=_open_pattern(bitstring), **kw)
     try:
         return eng(bitstring)
     finally:

@@ -150,3 +150,25 @@ def test_greedy_slice_invariants():
         prev = ws
     asg = list(iter_slice_assignments(tn, a))
     assert len(asg) == a.d and asg[3] == slice_assignment(tn, a, 3)
+
+
+def test_amplitude_projection_open_markers():
+    """_project fixes digits and keeps 'x' / '*' positions as outputs in qubit
+    order (host logic only)."""
+    import numpy as np
+    from paper_2002_01935_b200.executor import _project
+    from paper_2002_01935_b200.network import TensorNetwork, TensorNode
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((2, 2, 3)) + 0j
+    b = rng.standard_normal((2, 3)) + 0j
+    tn = TensorNetwork([TensorNode(0, ["q0", "q1", "k"], a), TensorNode(1, ["q2", "k"], b)],
+                       {"q0": 2, "q1": 2, "q2": 2, "k": 3}, ("q0", "q1", "q2"))
+    p = _project(tn, "x1*")
+    assert p.output == ("q0", "q2")
+    assert p.node(0).indices == ("q0", "k") and p.node(1).indices == ("q2", "k")
+    assert np.array_equal(p.node(0).data, a[:, 1, :])
+    assert "q1" not in p.index_table
+    with pytest.raises(ValueError):
+        _project(tn, "x1")
+    with pytest.raises(ValueError):
+        _project(tn, "a10")

@@ -547,3 +547,38 @@ def test_stacked_parent_fed_by_direct_children():
     # round (TNX_GEMM_FIRST), so allow ~2e-6 per GEMM (north star: 1e-5)
     for v in vals:
         assert rel_err(v, ref) <= 5e-6
+
+
+def test_amplitude_open_qubits_batch():
+    """Bitstrings with open qubits ('x'): one contraction returns the
+    amplitudes of all 2^N_f completions (PAPER.md N_f open qubits), equal to
+    the individual full-bitstring amplitudes and the oracle."""
+    from paper_2002_01935_b200.executor import _project, amplitude
+    tn = gen.grid_circuit(2, 3, 6, seed=4, simplify=False)
+    nodes, out = [], []
+    for nd in tn.nodes:
+        if len(nd.indices) == 1 and nd.id >= len(tn.nodes) - 6:
+            out.append(nd.indices[0])
+            continue
+        nodes.append(nd)
+    open_tn = TensorNetwork([TensorNode(i, nd.indices, nd.data) for i, nd in enumerate(nodes)],
+                            tn.index_table, tuple(out))
+    pattern = "0x1x00"
+    ptn = _project(open_tn, pattern)
+    tree = greedy_tree(ptn)
+    eng = AmplitudeEngine(open_tn, tree, open_qubits=pattern)
+    batch = np.asarray(eng(pattern))
+    assert batch.shape == (2, 2)
+    ref, _, _ = oracle.contract(ptn, tree)
+    assert rel_err(batch, ref) <= TOL
+    with pytest.raises(ValueError):
+        eng("000000")
+    eng.close()
+    full_tree = greedy_tree(_project(open_tn, "0" * 6))
+    full = AmplitudeEngine(open_tn, full_tree)
+    for a in range(2):
+        for b in range(2):
+            c = full(f"0{a}1{b}00")
+            assert abs(batch[a, b] - c) <= 1e-5 * max(abs(c), 1e-3)
+    full.close()
+    assert np.allclose(np.asarray(amplitude(open_tn, pattern, tree)), batch, atol=1e-7)
