@@ -184,6 +184,17 @@ class _CircuitTN:
         self.tensors.append([[o2, self.wire[q2], k], B])
         self.wire[q1], self.wire[q2] = o1, o2
 
+    def gate1_diag(self, q, U):
+        """Diagonal single-qubit gate, diagonal-reduced: a
+        rank-1 node on the wire label, which is not advanced (hyperedge)."""
+        self.tensors.append([[self.wire[q]], np.diag(U).copy()])
+
+    def cz_diag(self, q1, q2):
+        """CZ diagonal-reduced: rank-2 node M[a, b] = (-1)^(a b) on the two
+        wire labels, which continue as hyperedges."""
+        M = np.array([[1.0, 1.0], [1.0, -1.0]], dtype=np.complex128)
+        self.tensors.append([[self.wire[q1], self.wire[q2]], M])
+
     def gate2(self, q1, q2, U4):
         o1, o2 = self._new(), self._new()
         self.tensors.append([[o1, o2, self.wire[q1], self.wire[q2]], U4.copy()])
@@ -195,8 +206,11 @@ class _CircuitTN:
             v[int(bitstring[q])] = 1.0
             self.tensors.append([[self.wire[q]], v])
 
-    def simplify(self):
-        """Absorb every rank<=2 tensor into its highest-rank neighbour."""
+    def simplify(self, hyper=False):
+        """Absorb every rank<=2 tensor into its highest-rank neighbour.  With
+        hyperedges (diagonal-reduced circuits) only into a neighbour that
+        already carries all its labels, so no rank grows (rank-simplification,
+        PAPER.md §III.G)."""
         ts = [t for t in self.tensors]
         alive = list(range(len(ts)))
         holders = {}
@@ -214,13 +228,18 @@ class _CircuitTN:
                 for lbl in labels:
                     nbrs |= holders[lbl]
                 nbrs.discard(i)
+                if hyper:
+                    nbrs = {t for t in nbrs if set(labels) <= set(ts[t][0])}
                 if not nbrs:
                     continue
                 j = max(nbrs, key=lambda t: (len(ts[t][0]), -t))
                 la, A = ts[i]
                 lb, B = ts[j]
                 shared = [l for l in la if l in lb]
-                outl = [l for l in lb if l not in shared] + [l for l in la if l not in shared]
+                # a shared label carried by other tensors too (hyperedge) stays
+                # as a batch label; only labels private to i and j are summed
+                summed = [l for l in shared if holders[l] <= {i, j}]
+                outl = [l for l in lb if l not in summed] + [l for l in la if l not in summed and l not in lb]
                 sym = {}
                 for l in la + lb:
                     sym.setdefault(l, chr(97 + len(sym)))
@@ -298,8 +317,11 @@ def _grid_ops(rows, cols, depth, seed):
     return nq, ops
 
 
-def grid_circuit(rows, cols, depth, seed=0, bitstring=None, simplify=True):
-    """Amplitude network <x|U|0^N> of a GRCS-style rows x cols circuit."""
+def grid_circuit(rows, cols, depth, seed=0, bitstring=None, simplify=True, diag=False):
+    """Amplitude network <x|U|0^N> of a GRCS-style rows x cols circuit.
+    ``diag=True`` diagonal-reduces CZ and T gates (PAPER.md
+    §III.G): their wires continue as hyperedges instead of being split, the
+    hyperedge-heavy form the paper's JAX executor handled poorly."""
     nq, ops = _grid_ops(rows, cols, depth, seed)
     bitstring = "0" * nq if bitstring is None else bitstring
     if len(bitstring) != nq:
@@ -307,12 +329,17 @@ def grid_circuit(rows, cols, depth, seed=0, bitstring=None, simplify=True):
     c = _CircuitTN(nq)
     for op in ops:
         if op[0] == "1":
-            c.gate1(op[1], _SQ[op[2]])
+            if diag and op[2] == "T":
+                c.gate1_diag(op[1], _SQ[op[2]])
+            else:
+                c.gate1(op[1], _SQ[op[2]])
+        elif diag:
+            c.cz_diag(op[1], op[2])
         else:
             c.cz(op[1], op[2])
     c.close(bitstring)
     if simplify:
-        c.simplify()
+        c.simplify(hyper=diag)
     return c.network()
 
 

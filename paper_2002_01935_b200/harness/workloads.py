@@ -37,6 +37,12 @@ CONFIGS = {
                           desc="7x7 (1+20+1) circuit amplitude (parity companion of cfg4)"),
     "cfg5_syc53_m12": dict(make=lambda: gen.sycamore_circuit(12, seed=0), ws=27,
                            desc="Sycamore-like 53-qubit m=12 circuit amplitude, synthetic fSim"),
+    # the cfg4 circuit diagonal-reduced (CZ and T gates as hyperedge nodes,
+    # SPEC.md:241-248): hyperedge-heavy networks (batched GEMM / SIMT paths)
+    "cfg4d_7x7_d40_diag": dict(make=lambda: gen.grid_circuit(7, 7, 40, seed=0, diag=True), ws=27,
+                               desc="7x7 (1+40+1) circuit amplitude, diagonal-reduced (hyperedges)"),
+    "cfg4dp_7x7_d20_diag": dict(make=lambda: gen.grid_circuit(7, 7, 20, seed=0, diag=True), ws=None,
+                                desc="7x7 (1+20+1) diagonal-reduced amplitude (parity: equals cfg4p_7x7_d20)"),
 }
 
 

@@ -15,6 +15,8 @@ pytestmark = pytest.mark.gpu
 
 CASES = [("cfg1_3reg50", None, 3), ("cfg2_5reg100", 24, 3), ("cfg3_lattice20", None, 1),
          ("cfg3_lattice20", 21, 3), ("cfg4_7x7_d40", 27, 1), ("cfg5_syc53_m12", 24, 3)]
+# (the diagonal-reduced cfg4d network is covered at depth 20 below: the CPU
+#  oracle's hyperedge contractions at depth 40 / W_s=24 take ~10 minutes)
 
 
 def _root_check(tn, tree, ss, plan, s):
@@ -64,6 +66,27 @@ def test_full_amplitude_matches_oracle(name, ws):
     depths the CPU oracle contracts unsliced: relative error <= 1e-5."""
     tn, tree, ss, meta = load_workload(name, ws=ws)
     ref, _, ops_ref = oracle.contract(tn, tree)
+    plan = SlicedPlan(tn, tree, ss).bind()
+    try:
+        plan.run()
+        got = complex(plan.result())
+    finally:
+        plan.close()
+    assert abs(got - ref) <= 1e-5 * abs(ref), (got, ref, abs(got - ref) / abs(ref))
+
+
+@pytest.mark.parametrize("ws", [None, 16])
+def test_diagonal_reduced_amplitude_equals_split(ws):
+    """The same 7x7 (1+20+1) circuit built with diagonal reduction (CZ / T as
+    hyperedge nodes, 193+ hyperedges) and with spatially split CZs: the GPU
+    amplitude of the hyperedge network (unsliced and sliced) equals the
+    oracle's amplitude of both forms."""
+    tn, tree, ss, meta = load_workload("cfg4dp_7x7_d20_diag", ws=ws)
+    assert sum(1 for l in tn.index_table if sum(l in nd.indices for nd in tn.nodes) > 2) > 100
+    ref, _, _ = oracle.contract(tn, tree)
+    tn2, tree2, _, _ = load_workload("cfg4p_7x7_d20")
+    ref_split, _, _ = oracle.contract(tn2, tree2)
+    assert abs(ref - ref_split) <= 1e-10 * abs(ref_split)
     plan = SlicedPlan(tn, tree, ss).bind()
     try:
         plan.run()
