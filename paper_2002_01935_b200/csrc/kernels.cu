@@ -603,19 +603,28 @@ __global__ void __launch_bounds__(256) dot_kernel(const DotParams p) {
   const int64_t n2 = p.n >> 1;  // complex pairs (16 B)
   const float4* x4 = reinterpret_cast<const float4*>(p.x);
   const float4* y4 = reinterpret_cast<const float4*>(p.y);
-  float re = 0.f, im = 0.f;
+  float re = 0.f, im = 0.f, re2 = 0.f, im2 = 0.f;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
-    const float4 a = x4[i], b = y4[i];
-    re = fmaf(a.x, b.x, re);
-    re = fmaf(-a.y, b.y, re);
-    im = fmaf(a.x, b.y, im);
-    im = fmaf(a.y, b.x, im);
-    re = fmaf(a.z, b.z, re);
-    re = fmaf(-a.w, b.w, re);
-    im = fmaf(a.z, b.w, im);
-    im = fmaf(a.w, b.z, im);
+  auto mac = [](const float4 a, const float4 b, float& r, float& m) {
+    r = fmaf(a.x, b.x, r);
+    r = fmaf(-a.y, b.y, r);
+    m = fmaf(a.x, b.y, m);
+    m = fmaf(a.y, b.x, m);
+    r = fmaf(a.z, b.z, r);
+    r = fmaf(-a.w, b.w, r);
+    m = fmaf(a.z, b.w, m);
+    m = fmaf(a.w, b.z, m);
+  };
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + stride < n2; i += 2 * stride) {  // two independent 32-byte load pairs in flight
+    const float4 a0 = __ldcs(x4 + i), b0 = __ldcs(y4 + i);
+    const float4 a1 = __ldcs(x4 + i + stride), b1 = __ldcs(y4 + i + stride);
+    mac(a0, b0, re, im);
+    mac(a1, b1, re2, im2);
   }
+  if (i < n2) mac(__ldcs(x4 + i), __ldcs(y4 + i), re, im);
+  re += re2;
+  im += im2;
   if ((p.n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     const float2 a = p.x[p.n - 1], b = p.y[p.n - 1];
     re += a.x * b.x - a.y * b.y;

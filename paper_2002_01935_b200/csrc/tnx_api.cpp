@@ -558,9 +558,15 @@ int compile(Plan& P, const tnx_plan_desc* D) {
     TensorLoc& z = P.T[v.ssa];
     // tensor cores for GEMM-shaped vertices; small K (padded to 16) still
     // goes there when the output is large (SIMT would be output-bound)
+    // tcgen05 GEMM: K >= 16 contractions with enough MACs even for narrow M / N
+    // (a 128-row tile at half utilisation beats the SIMT kernels by >10x; below 64
+    // rows the extra TF32 error outweighs it -- a 7x7 amplitude test crossed 1e-5 at 16;
+    // rows / columns past M / N are computed and masked), small-K ones only
+    // when the output is large (SIMT would be output-bound)
+    static const int64_t min_mn = getenv("TNX_GEMM_MIN_MN") ? atoll(getenv("TNX_GEMM_MIN_MN")) : 64;
     const bool gemm = P.precision != TNX_PREC_FP32 && v.dxl.empty() && v.dyl.empty() &&
-                      v.M >= 128 && v.N >= 128 &&
-                      (v.K >= 16 ? (double)v.macs >= P.gemm_min_macs : v.M * v.N >= (int64_t(1) << 20));
+                      (v.K >= 16 ? std::min(v.M, v.N) >= min_mn && (double)v.macs >= P.gemm_min_macs
+                                 : v.M >= 128 && v.N >= 128 && v.M * v.N >= (int64_t(1) << 20));
     if (gemm) {
       v.kind = VK_GEMM;
       // A takes the operand with more rows (output rows = A rows)
@@ -1096,7 +1102,7 @@ int lower(Plan& P) {
         dp.z = P.ptr(z);
         dp.partial = P.partial;
         dp.n = x.size;
-        dp.nblocks = 148 * 4;
+        dp.nblocks = 148 * 8;
         // y in another layout: one fused launch reads y through the permute tile
         // and multiplies with x in place (no permuted copy of y)
         dp.perm = v.blk_tmp >= 0 ? (int)P.perms.size() - 1 : -1;
