@@ -73,15 +73,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
   } while (!done);
 }
 
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, uint32_t mbar, int c0,
-                                            int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(mbar), "r"(c0), "r"(c1)
-      : "memory");
-}
-
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* tmap, uint32_t mbar, int c0,
                                             int c1, int c2) {
   asm volatile(
@@ -101,12 +92,6 @@ __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
   d |= (uint64_t)1u << 46;
   d |= (uint64_t)4u << 61;
   return d;
-}
-
-// Instruction descriptor: D=f32, A=B=tf32, K-major both, N=128, M=128.
-__host__ __device__ constexpr uint32_t idesc_tf32(bool neg_a) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((neg_a ? 1u : 0u) << 13) |
-         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
 __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
@@ -141,16 +126,6 @@ __device__ __forceinline__ void tc_fence_before() {
 }
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
@@ -242,23 +217,23 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& g, float2* out, i
           store_mix_x(d + ps, off + t, mre[j + t], g.dside);
           store_mix_x(d + 3 * ps, off + t, mim[j + t], g.dside);
         }
-        continue;
-      }
-      float rh[4], rl[4], ih[4], il[4];
+      } else {
+        float rh[4], rl[4], ih[4], il[4];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        rh[t] = __uint_as_float(__float_as_uint(mre[j + t]) & 0xffffe000u);
-        ih[t] = __uint_as_float(__float_as_uint(mim[j + t]) & 0xffffe000u);
-        rl[t] = mre[j + t] - rh[t];
-        il[t] = mim[j + t] - ih[t];
-      }
-      *reinterpret_cast<float4*>(d + off) = make_float4(rh[0], rh[1], rh[2], rh[3]);
-      *reinterpret_cast<float4*>(d + off + ps) = make_float4(rl[0], rl[1], rl[2], rl[3]);
-      *reinterpret_cast<float4*>(d + off + 2 * ps) = make_float4(ih[0], ih[1], ih[2], ih[3]);
-      *reinterpret_cast<float4*>(d + off + 3 * ps) = make_float4(il[0], il[1], il[2], il[3]);
-      if (g.dstack) {
-        *reinterpret_cast<float4*>(d + off + 4 * ps) = make_float4(-ih[0], -ih[1], -ih[2], -ih[3]);
-        *reinterpret_cast<float4*>(d + off + 5 * ps) = make_float4(-il[0], -il[1], -il[2], -il[3]);
+        for (int t = 0; t < 4; ++t) {
+          rh[t] = __uint_as_float(__float_as_uint(mre[j + t]) & 0xffffe000u);
+          ih[t] = __uint_as_float(__float_as_uint(mim[j + t]) & 0xffffe000u);
+          rl[t] = mre[j + t] - rh[t];
+          il[t] = mim[j + t] - ih[t];
+        }
+        *reinterpret_cast<float4*>(d + off) = make_float4(rh[0], rh[1], rh[2], rh[3]);
+        *reinterpret_cast<float4*>(d + off + ps) = make_float4(rl[0], rl[1], rl[2], rl[3]);
+        *reinterpret_cast<float4*>(d + off + 2 * ps) = make_float4(ih[0], ih[1], ih[2], ih[3]);
+        *reinterpret_cast<float4*>(d + off + 3 * ps) = make_float4(il[0], il[1], il[2], il[3]);
+        if (g.dstack) {
+          *reinterpret_cast<float4*>(d + off + 4 * ps) = make_float4(-ih[0], -ih[1], -ih[2], -ih[3]);
+          *reinterpret_cast<float4*>(d + off + 5 * ps) = make_float4(-il[0], -il[1], -il[2], -il[3]);
+        }
       }
     }
     return;
@@ -301,14 +276,6 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& g, float2* out, i
     for (int j = 0; j < 64; ++j)
       if (col0 + j < g.N) orow[col0 + j] = make_float2(mre[j], mim[j]);
   }
-}
-
-// Column-offset table of this CTA's 128 output columns (direct mode); called
-// by all 256 epilogue threads after the last accumulator round.
-__device__ __forceinline__ void build_gtab(const GemmArgs& g, int64_t* gtab, int64_t col_base) {
-  const int e = threadIdx.x - 64;
-  if (e < BN) gtab[e] = (col_base + e < g.N) ? map_offset(g.gmap, col_base + e) : 0;
-  asm volatile("bar.sync 1, 256;" ::: "memory");
 }
 
 // TMEM-set release by the epilogue warps.  Relaxed: the MMA issuer only needs

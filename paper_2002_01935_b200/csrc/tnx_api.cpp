@@ -306,17 +306,6 @@ bool build_map(const Plan& P, const std::vector<int>& labels, const TensorLoc* t
   return true;
 }
 
-std::string u128_str(u128 v) {
-  if (v == 0) return "0";
-  std::string s;
-  while (v) {
-    s.push_back(char('0' + int(v % 10)));
-    v /= 10;
-  }
-  std::reverse(s.begin(), s.end());
-  return s;
-}
-
 // Label order of the K-blocked operand planes of GEMM vertex v, side 0 (A)
 // or 1 (B): row-major [K outer][batch + side rows][K inner, product 16].
 // False when K is padded or no K suffix has product 16 (gather-pack path).
