@@ -1,6 +1,6 @@
 """Randomised parity sweep (GPU vs the complex128 oracle) over networks big
 enough to reach the tensor-core paths: 3/4-regular graphs, small grid
-circuits and hypergraph networks with open outputs, random greedy trees,
+circuits (split and diagonal-reduced) and hypergraph networks with open outputs, random greedy trees,
 random slicings, random precision / fusion options, lowered GEMM thresholds.
 
     python tools/fuzz_gpu.py [seconds] [first_seed]
@@ -27,8 +27,11 @@ from paper_2002_01935_b200.tree import metrics
 
 def make(seed):
     rng = np.random.default_rng(seed)
-    kind = seed % 3
-    if kind == 0:
+    kind = seed % 4
+    if kind == 3:  # diagonal-reduced circuit: hyperedge-heavy (batched GEMM / SIMT)
+        rows, cols = int(rng.integers(4, 7)), int(rng.integers(5, 8))
+        tn = gen.grid_circuit(rows, cols, int(rng.integers(10, 25)), seed=seed, diag=True)
+    elif kind == 0:
         n = int(rng.integers(60, 140)) // 2 * 2
         tn = gen.random_regular(n, int(rng.choice([3, 4])), seed=seed)
     elif kind == 1:
