@@ -454,7 +454,8 @@ __device__ __forceinline__ int perm_swz(int i) {
 
 constexpr int kPermMaxPairs = 4;  // (ts * group / 2) / 256 <= 2048 / 2 / 256 (vec needs ts <= 2048)
 
-__global__ void __launch_bounds__(256, 4) perm_vec_kernel(const PermParams p) {
+template <bool DOT>
+__global__ void __launch_bounds__(256, DOT ? 3 : 4) perm_vec_kernel(const PermParams p) {
   pdl_wait();
   extern __shared__ __align__(16) unsigned char perm_smem[];
   __shared__ int64_t base_s[2][64], base_d[2][64];
@@ -511,6 +512,19 @@ __global__ void __launch_bounds__(256, 4) perm_vec_kernel(const PermParams p) {
         tile[perm_swz((j << lg) + t_idx[t + 1])] = make_float2(r[i].z, r[i].w);
       }
     }
+    // fused dot: this chunk's x values (destination order, same e -> (j, t) map as
+    // the store phase) go in flight now, across the barrier and the next issue
+    float4 xr[kPermMaxPairs];
+    if constexpr (DOT) {
+#pragma unroll
+      for (int i = 0; i < kPermMaxPairs; ++i) {
+        const int e = threadIdx.x + i * 256;
+        if (e < npairs) {
+          const int j = e >> half_lg, t = (e & half_mask) << 1;
+          xr[i] = __ldcs(reinterpret_cast<const float4*>(p.dotx + base_d[buf][j] + t_dst[t]));
+        }
+      }
+    }
     const int64_t cn = c + gridDim.x;
     const bool more = cn < nchunks;
     if (more) bases(cn, buf ^ 1);
@@ -520,22 +534,29 @@ __global__ void __launch_bounds__(256, 4) perm_vec_kernel(const PermParams p) {
       npairs = count_of(cn) << half_lg;
       issue(buf ^ 1, npairs);
     }
-    for (int e = threadIdx.x; e < np_cur; e += blockDim.x) {
+    if constexpr (DOT) {  // fused dot: multiply the permuted tile with x in place
+#pragma unroll
+      for (int i = 0; i < kPermMaxPairs; ++i) {
+        const int e = threadIdx.x + i * 256;
+        if (e < np_cur) {
+          const int j = e >> half_lg, t = (e & half_mask) << 1;
+          const float4 v = *reinterpret_cast<const float4*>(tile + perm_swz((j << lg) + t));
+          const float4 xv = xr[i];
+          dre = fmaf(xv.x, v.x, dre);
+          dre = fmaf(-xv.y, v.y, dre);
+          dim = fmaf(xv.x, v.y, dim);
+          dim = fmaf(xv.y, v.x, dim);
+          dre = fmaf(xv.z, v.z, dre);
+          dre = fmaf(-xv.w, v.w, dre);
+          dim = fmaf(xv.z, v.w, dim);
+          dim = fmaf(xv.w, v.z, dim);
+        }
+      }
+    }
+    for (int e = threadIdx.x; !DOT && e < np_cur; e += blockDim.x) {
       const int j = e >> half_lg, t = (e & half_mask) << 1;
       const float4 v = *reinterpret_cast<const float4*>(tile + perm_swz((j << lg) + t));
       const int64_t off = base_d[buf][j] + t_dst[t];
-      if (p.mode == 5) {  // fused dot: multiply with the other operand in place
-        const float4 xv = __ldg(reinterpret_cast<const float4*>(p.dotx + off));
-        dre = fmaf(xv.x, v.x, dre);
-        dre = fmaf(-xv.y, v.y, dre);
-        dim = fmaf(xv.x, v.y, dim);
-        dim = fmaf(xv.y, v.x, dim);
-        dre = fmaf(xv.z, v.z, dre);
-        dre = fmaf(-xv.w, v.w, dre);
-        dim = fmaf(xv.z, v.w, dim);
-        dim = fmaf(xv.w, v.z, dim);
-        continue;
-      }
       if (p.mode == 0) {
         __stcs(reinterpret_cast<float4*>(static_cast<float2*>(p.dst) + off), v);
       } else {
@@ -565,7 +586,7 @@ __global__ void __launch_bounds__(256, 4) perm_vec_kernel(const PermParams p) {
     c = cn;
     buf ^= 1;
   }
-  if (p.mode == 5) perm_dot_reduce(dre, dim, p.partial);
+  if constexpr (DOT) perm_dot_reduce(dre, dim, p.partial);
 }
 
 cudaError_t launch_perm(const PermParams& p, cudaStream_t st) {
@@ -575,11 +596,15 @@ cudaError_t launch_perm(const PermParams& p, cudaStream_t st) {
   if (blocks < 1) blocks = 1;
   if (p.vec && p.ts * p.group <= 2048) {
     static bool carveout = [] {
-      cudaFuncSetAttribute(perm_vec_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      cudaFuncSetAttribute(perm_vec_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      cudaFuncSetAttribute(perm_vec_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       return true;
     }();
     (void)carveout;
-    launch_pdl(perm_vec_kernel, blocks, 256, smem, st, p);
+    if (p.mode == 5)
+      launch_pdl(perm_vec_kernel<true>, blocks, 256, smem, st, p);
+    else
+      launch_pdl(perm_vec_kernel<false>, blocks, 256, smem, st, p);
   }
   else
     launch_pdl(perm_kernel, blocks, 256, smem, st, p);
