@@ -65,3 +65,21 @@ def test_oracle_brute_force_random():
         tree = greedy_tree(tn, seed=seed)
         val, _, _ = oracle.contract(tn, tree)
         assert rel_err(val, oracle.brute_force(tn)) <= 1e-10
+
+
+@pytest.mark.parametrize("rows,cols,depth", [(3, 4, 10), (4, 4, 12)])
+def test_diagonal_reduced_circuit_amplitudes(rows, cols, depth):
+    """Diagonal-reduced circuits (CZ / T as hyperedge nodes, hyperedge-safe
+    rank simplification) give the statevector amplitude, like the split form."""
+    import numpy as np
+    from paper_2002_01935_b200.harness import generators as gen
+    from paper_2002_01935_b200.harness.paths import greedy_tree
+    for seed in range(2):
+        bits = "".join(str(b) for b in np.random.default_rng(seed).integers(0, 2, rows * cols))
+        ref = gen.circuit_statevector_amplitude(rows, cols, depth, seed=seed, bitstring=bits)
+        for simplify in (False, True):
+            tn = gen.grid_circuit(rows, cols, depth, seed=seed, bitstring=bits, simplify=simplify, diag=True)
+            if not simplify:
+                assert any(sum(l in nd.indices for nd in tn.nodes) > 2 for l in tn.index_table)
+            val, _, _ = oracle.contract(tn, greedy_tree(tn))
+            assert abs(val - ref) <= 1e-10 * max(1.0, abs(ref))
