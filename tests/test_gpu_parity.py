@@ -582,3 +582,29 @@ def test_amplitude_open_qubits_batch():
             assert abs(batch[a, b] - c) <= 1e-5 * max(abs(c), 1e-3)
     full.close()
     assert np.allclose(np.asarray(amplitude(open_tn, pattern, tree)), batch, atol=1e-7)
+
+
+def test_amplitude_open_qubits_sliced():
+    """Open qubits together with slicing: the (2, 2) amplitude tensor summed
+    over slices (output permutation + tensor-valued accumulation) equals the
+    unsliced oracle."""
+    from paper_2002_01935_b200.executor import _project, amplitude
+    tn = gen.grid_circuit(3, 4, 8, seed=6, simplify=False)
+    nq = 12
+    nodes, out = [], []
+    for nd in tn.nodes:
+        if len(nd.indices) == 1 and nd.id >= len(tn.nodes) - nq:
+            out.append(nd.indices[0])
+            continue
+        nodes.append(nd)
+    open_tn = TensorNetwork([TensorNode(i, nd.indices, nd.data) for i, nd in enumerate(nodes)],
+                            tn.index_table, tuple(out))
+    pattern = "x0110100101x"
+    ptn = _project(open_tn, pattern)
+    tree = best_greedy_tree(ptn, trials=2)
+    ss = greedy_slice(tree, ptn, metrics(tree, ptn).width - 2, restarts=1)
+    assert ss.d > 1
+    got = np.asarray(amplitude(open_tn, pattern, tree, ss))
+    ref, _, _ = oracle.contract(ptn, tree)
+    assert got.shape == (2, 2)
+    assert rel_err(got, ref) <= TOL
