@@ -194,7 +194,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     tn, tree, ss, meta = workload(args)
-    from paper_2002_01935_b200.tree import annotate_incidence
+    from paper_2002_01935_b200.refpkg import annotate_incidence
     annotate_incidence(tree, tn)
     import oracle
     per_slice = oracle.width_cost(tn, tree, ss.labels)[1]

@@ -5,28 +5,29 @@ This module is the checker, never the product: only ``tests/``,
 ``--impl reference`` legs may import it.  The B200 product path
 (``paper_2002_01935_b200``) never imports or calls anything here.
 
-It restates, in complex128 numpy, the executor that the reference specifies
-(`/root/reference/SPEC.md:510-558`, ``contract`` / ``contract_sliced``) on top
-of the reference's own per-op semantics:
+The reference ships the per-op building blocks but not the executor loop
+(`/root/reference/SPEC.md:510-558`, ``contract`` / ``contract_sliced`` are
+spec-only).  This oracle is that loop, written over the REFERENCE'S OWN
+functions, called directly from the installed ``hypertn`` (``baseline/_ref``,
+located by ``paper_2002_01935_b200.refpkg``):
 
-* keep sets   -- the label-count saturation rule of ``HyperView.merge_counts``
-  (`/root/reference/pkg/src/hypertn/hypergraph.py:106-119`) as driven by
-  ``annotate_incidence`` (`tree.py:137-169`), appearances from
-  ``HyperView.from_network`` (`hypergraph.py:39-57`);
-* per-pair op -- ``pairwise_contract`` (`dense.py:61-76`): shared-dim check,
-  output labels = x's kept labels then y's new kept labels, evaluated with
-  ``np.einsum(..., optimize=True)`` exactly as ``_einsum_pair`` (`dense.py:47-58`);
-* op count    -- ``union_product`` (`hypergraph.py:121-131`) per vertex;
-* slicing     -- ``fix_index`` (`dense.py:161-170`) on every leaf carrying a
-  sliced label; slice ids enumerate mixed-radix, last label fastest
-  (SURVEY.md §8(a) a14);
+* keep sets   -- ``hypertn.tree.annotate_incidence`` (`tree.py:137-169`), i.e.
+  the saturation rule of ``HyperView.merge_counts`` (`hypergraph.py:106-119`);
+* per-pair op -- ``hypertn.dense.pairwise_contract`` (`dense.py:61-76`, which
+  evaluates ``np.einsum(..., optimize=True)``, `dense.py:47-58`).  Only a pair
+  whose label union exceeds the reference's 52-symbol limit (`dense.py:10`,
+  `:49-52`) -- which the reference itself cannot contract -- goes through the
+  restated batch/M/N/K matmul ``_matmul_pair`` below;
+* op count    -- the union product (`hypergraph.py:121-131`) per vertex;
+* slicing     -- ``hypertn.dense.fix_index`` (`dense.py:161-170`) on every
+  leaf carrying a sliced label; slice ids enumerate mixed-radix, last label
+  fastest (SURVEY.md §8(a) a14);
 * root        -- ``DenseTensor.transpose_to(tn.output)`` (`dense.py:36-41`);
 * reduction   -- compensated (Kahan) complex128 summation over slices
   (SPEC.md:551); ``strip_exponent`` renormalisation (SPEC.md:518).
 
-Parity pinning: ``tests/golden/make_golden.py`` runs the REAL reference
-functions (imported from /root/reference in the build container) on seeded
-networks and commits their outputs as ``tests/golden/*.json``;
+Parity pinning: ``tests/golden/make_golden.py`` records outputs of the
+reference functions on seeded networks as ``tests/golden/*.json``;
 ``tests/test_oracle_golden.py`` checks this oracle against them.
 """
 
@@ -36,6 +37,8 @@ import math
 import string
 
 import numpy as np
+
+from paper_2002_01935_b200.refpkg import dense as _rd, annotate_incidence as _annotate
 
 _LETTERS = string.ascii_letters  # dense.py:10 -- at most 52 labels per pair
 
@@ -53,26 +56,11 @@ def appearances(tn):
 
 
 def vertex_terms(tn, tree):
-    """Ordered {label: count} per SSA vertex (tree.py:155-166)."""
-    app = appearances(tn)
-    by_id = {nd.id: nd for nd in tn.nodes}
-    n = len(tree.leaves)
-    terms = []
-    for nid in tree.leaves:
-        terms.append({lbl: 1 for lbl in by_id[nid].indices})
-    for a, b in tree.pairs:
-        ta, tb = terms[a], terms[b]
-        merged = {}
-        for lbl, c in ta.items():
-            c2 = c + tb.get(lbl, 0)
-            if c2 < app[lbl]:
-                merged[lbl] = c2
-        for lbl, c in tb.items():
-            if lbl not in ta and c < app[lbl]:
-                merged[lbl] = c
-        terms.append(merged)
-    assert len(terms) == (2 * n - 1 if n > 1 else 1)
-    return terms
+    """Ordered {label: count} per SSA vertex, from the reference's
+    ``annotate_incidence`` (tree.py:137-169)."""
+    _annotate(tree, tn)
+    names = tree._ann.view.labels
+    return [{names[li]: c for li, c in cnt.items()} for cnt in tree._ann.counts]
 
 
 def cost_terms(tn, tree, sliced=()):
@@ -111,19 +99,6 @@ def width_cost(tn, tree, sliced=()):
 
 
 # --------------------------------------------------------------- numerics
-def _einsum_pair(xl, x, yl, y, outl):
-    if len(set(xl) | set(yl)) <= len(_LETTERS):
-        sym = {}
-        for lbl in (*xl, *yl):
-            if lbl not in sym:
-                sym[lbl] = _LETTERS[len(sym)]
-        sub = "{},{}->{}".format("".join(sym[l] for l in xl),
-                                 "".join(sym[l] for l in yl),
-                                 "".join(sym[l] for l in outl))
-        return np.einsum(sub, x, y, optimize=True)
-    return _matmul_pair(xl, x, yl, y, outl)
-
-
 def _matmul_pair(xl, x, yl, y, outl):
     """Same math as einsum without the 52-label limit (batch/M/N/K grouping)."""
     xs, ys, os_ = set(xl), set(yl), set(outl)
@@ -154,24 +129,23 @@ def _matmul_pair(xl, x, yl, y, outl):
 
 
 def pairwise_contract(xl, x, yl, y, keep):
-    """Reference ``pairwise_contract`` semantics (dense.py:61-76)."""
+    """The reference's ``pairwise_contract`` (dense.py:61-76) on labelled
+    arrays; the restated matmul form only past its 52-label limit."""
+    if len(set(xl) | set(yl)) <= len(_LETTERS):
+        t = _rd.pairwise_contract(_rd.DenseTensor(xl, x), _rd.DenseTensor(yl, y), keep)
+        return tuple(t.labels), t.array
     for i, lbl in enumerate(xl):
         if lbl in yl and x.shape[i] != y.shape[yl.index(lbl)]:
             raise ValueError(f"dim mismatch on shared index {lbl}")
     outl = [l for l in xl if l in keep]
     outl += [l for l in yl if l in keep and l not in xl]
-    return tuple(outl), _einsum_pair(list(xl), x, list(yl), y, outl)
+    return tuple(outl), _matmul_pair(list(xl), x, list(yl), y, outl)
 
 
 def fix_index(labels, arr, label, value):
-    """Reference ``fix_index`` (dense.py:161-170)."""
-    ax = list(labels).index(label)
-    d = arr.shape[ax]
-    if not 0 <= value < d:
-        raise ValueError(f"value {value} out of range for dim {d} index {label}")
-    idx = [slice(None)] * arr.ndim
-    idx[ax] = value
-    return tuple(labels[:ax]) + tuple(labels[ax + 1:]), arr[tuple(idx)]
+    """The reference's ``fix_index`` (dense.py:161-170)."""
+    t = _rd.fix_index(_rd.DenseTensor(labels, arr), label, value)
+    return tuple(t.labels), t.array
 
 
 def slice_digits(dims, s):
@@ -235,8 +209,7 @@ def contract_one(tn, tree, sliced=(), assignment=None, strip_exponent=False,
     if extra:
         r = r.sum(axis=tuple(rl.index(l) for l in extra))
         rl = tuple(l for l in rl if l not in extra)
-    if tuple(rl) != tuple(out):
-        r = np.transpose(r, [rl.index(l) for l in out])
+    r = _rd.DenseTensor(rl, r).transpose_to(out).array
     return np.asarray(r, dtype=np.complex128), exp10, ops, peak
 
 

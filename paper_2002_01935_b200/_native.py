@@ -112,7 +112,7 @@ def check(rc):
         if rc in (TNX_ERR_INVALID, TNX_ERR_STATE):
             raise ValueError(msg)
         if rc == TNX_ERR_DATA:
-            from .network import DataError
+            from .refpkg import DataError
             raise DataError(msg)
         if rc == TNX_ERR_NUMERIC:
             raise FloatingPointError(msg)

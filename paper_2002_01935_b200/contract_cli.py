@@ -33,8 +33,8 @@ def result_document(value, exponent10, op_count, plan_stats, slices_run):
 
 
 def main(argv=None):
-    from .network import DataError, load_network
-    from .tree import tree_from_path_dict
+    from .refpkg import DataError, load_network
+    from .refpkg import tree_from_path_dict
     from .slicing import SliceSet, greedy_slice
     from .executor import SlicedPlan, _finish
 

@@ -26,7 +26,7 @@ import threading
 import numpy as np
 
 from . import _native as nat
-from .network import DataError, TensorNetwork, TensorNode
+from .refpkg import DataError, TensorNetwork, TensorNode
 
 __all__ = ["SlicedPlan", "contract", "contract_sliced", "amplitude", "AmplitudeEngine",
            "allreduce_plans", "PRECISIONS"]
@@ -281,11 +281,10 @@ class SlicedPlan:
         return labels, (buf[0::2] + 1j * buf[1::2]).astype(np.complex64).reshape(shape)
 
     def _vertex_size(self, v):
-        from .tree import annotate_incidence
-        annotate_incidence(self.tree, self.tn)
+        from .refpkg import ordered_labels
         size = 1
         S = set(self.sliced)
-        for lbl in self.tree._ann.ordered_labels(v):
+        for lbl in ordered_labels(self.tree, self.tn, v):
             if lbl not in S:
                 size *= self.tn.index_table[lbl]
         return size

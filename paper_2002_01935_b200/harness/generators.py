@@ -28,7 +28,7 @@ import math
 
 import numpy as np
 
-from ..network import TensorNetwork, TensorNode
+from ..refpkg import TensorNetwork, TensorNode
 
 __all__ = ["random_regular_graph", "random_regular", "square_lattice",
            "grid_circuit", "sycamore_circuit", "random_hyper_network",

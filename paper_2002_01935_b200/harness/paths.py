@@ -17,7 +17,7 @@ import math
 
 import numpy as np
 
-from ..tree import ContractionTree, LabelAlgebra
+from ..refpkg import ContractionTree, HyperView
 
 __all__ = ["greedy_tree", "best_greedy_tree", "linear_tree"]
 
@@ -30,12 +30,12 @@ def greedy_tree(tn, seed=0, temperature=0.0, alpha=1.0):
     """Agglomerative greedy: merge the adjacent pair with the smallest
     2^out - alpha (2^a + 2^b); optional Gumbel noise of scale ``temperature``
     on the log-score for randomised restarts."""
-    alg = LabelAlgebra(tn)
-    n = len(alg.leaf_terms)
+    alg = HyperView.from_network(tn)
+    n = len(alg.terms)
     if n == 1:
         return ContractionTree(tn.node_ids, [])
     rng = np.random.default_rng(seed)
-    terms = {i: alg.leaf_terms[i] for i in range(n)}
+    terms = {i: alg.terms[i] for i in range(n)}
     lab2 = {}
     for i, t in terms.items():
         for li in t:
@@ -45,7 +45,7 @@ def greedy_tree(tn, seed=0, temperature=0.0, alpha=1.0):
     heap = []
 
     def score(a, b):
-        out = alg.merge(terms[a], terms[b])
+        out = alg.merge_counts(terms[a], terms[b])
         s = 2.0 ** min(1000, _log2size(alg, out)) - alpha * (
             2.0 ** min(1000, _log2size(alg, terms[a])) + 2.0 ** min(1000, _log2size(alg, terms[b])))
         if temperature > 0:
@@ -74,7 +74,7 @@ def greedy_tree(tn, seed=0, temperature=0.0, alpha=1.0):
             ks = sorted(terms, key=lambda f: (_log2size(alg, terms[f]), f))
             pick = (min(ks[0], ks[1]), max(ks[0], ks[1]))
         a, b = pick
-        merged = alg.merge(terms[a], terms[b])
+        merged = alg.merge_counts(terms[a], terms[b])
         for f in (a, b):
             for li in terms[f]:
                 lab2[li].discard(f)
@@ -89,7 +89,7 @@ def greedy_tree(tn, seed=0, temperature=0.0, alpha=1.0):
 
 
 def best_greedy_tree(tn, trials=8, seed=0, target="cost"):
-    from ..tree import metrics
+    from ..refpkg import metrics
     best, best_key = None, None
     for t in range(trials):
         tree = greedy_tree(tn, seed=seed + t, temperature=0.0 if t == 0 else 0.3)

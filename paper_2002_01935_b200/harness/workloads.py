@@ -15,7 +15,7 @@ import os
 from . import generators as gen
 from .paths import best_greedy_tree
 from ..slicing import greedy_slice, SliceSet
-from ..tree import ContractionTree, metrics
+from ..refpkg import ContractionTree, metrics
 
 REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 BENCHDATA = os.path.join(REPO, "benchdata")

@@ -27,7 +27,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .tree import annotate_incidence
+from .refpkg import annotate_incidence
 
 __all__ = ["SliceSet", "sliced_metrics", "sliced_cost_terms", "greedy_slice",
            "slice_assignment", "slice_digits", "iter_slice_assignments"]
@@ -81,13 +81,13 @@ class _MaskView:
     def __init__(self, tree, tn):
         annotate_incidence(tree, tn)
         ann = tree._ann
-        alg = ann.algebra
+        alg = ann.view
         self.alg = alg
         self.n = tree.n
         self.dims = alg.dims
         self.all_two = all(d == 2 for d in alg.dims)
         masks = []
-        for t in ann.terms:
+        for t in ann.counts:
             m = 0
             for li in t:
                 m |= 1 << li
@@ -253,7 +253,7 @@ def auto_slice(tree, tn, device_bytes, ws_max=None, ws_min=None, fill=0.9, resta
     ``fill * device_bytes``.  Larger W_s means fewer, larger slices and a lower
     total cost C_s.  Returns (SliceSet, plan_bytes)."""
     from .executor import SlicedPlan
-    from .tree import metrics
+    from .refpkg import metrics
     m = metrics(tree, tn)
     hi = int(math.floor(m.width if ws_max is None else min(ws_max, m.width)))
     lo = int(ws_min) if ws_min is not None else 1

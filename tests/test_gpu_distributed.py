@@ -25,7 +25,7 @@ def _case():
     from paper_2002_01935_b200.harness import generators as gen
     from paper_2002_01935_b200.harness.paths import best_greedy_tree
     from paper_2002_01935_b200.slicing import greedy_slice
-    from paper_2002_01935_b200.tree import metrics
+    from paper_2002_01935_b200.refpkg import metrics
     tn = gen.random_regular(30, 3, seed=9)
     # two open legs, so the all-reduce carries a tensor, not a scalar
     tn = tn.replace(output=tuple(list(tn.index_table)[:2]))

@@ -10,11 +10,11 @@ from conftest import arr_from_json, golden_cases
 from _util import case_objects, rel_err
 from paper_2002_01935_b200.executor import (SlicedPlan, contract, contract_sliced,
                                             AmplitudeEngine)
-from paper_2002_01935_b200.network import TensorNetwork, TensorNode
+from paper_2002_01935_b200.refpkg import TensorNetwork, TensorNode
 from paper_2002_01935_b200.harness import generators as gen
 from paper_2002_01935_b200.harness.paths import best_greedy_tree, greedy_tree
 from paper_2002_01935_b200.slicing import greedy_slice
-from paper_2002_01935_b200.tree import metrics
+from paper_2002_01935_b200.refpkg import metrics
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-5
@@ -207,7 +207,7 @@ def _two_tensor_net(xl, yl, out, seed=0):
     tab = {l: 2 for l in labels}
     x = (rng.standard_normal((2,) * len(xl)) + 1j * rng.standard_normal((2,) * len(xl))) / 2 ** (len(xl) / 4)
     y = (rng.standard_normal((2,) * len(yl)) + 1j * rng.standard_normal((2,) * len(yl))) / 2 ** (len(yl) / 4)
-    from paper_2002_01935_b200.tree import ContractionTree
+    from paper_2002_01935_b200.refpkg import ContractionTree
     tn = TensorNetwork([TensorNode(0, xl, x), TensorNode(1, yl, y)], tab, tuple(out))
     return tn, ContractionTree((0, 1), [(0, 1)])
 
@@ -242,8 +242,8 @@ def test_small_k_contraction_on_tensor_cores():
 
 def test_contract_cli_json(tmp_path):
     import json
-    from paper_2002_01935_b200.network import save_network
-    from paper_2002_01935_b200.tree import tree_to_path_dict
+    from paper_2002_01935_b200.refpkg import save_network
+    from paper_2002_01935_b200.refpkg import tree_to_path_dict
     from paper_2002_01935_b200.contract_cli import main
     tn = gen.grid_circuit(4, 4, 10, seed=3)
     tree = best_greedy_tree(tn, trials=2)
@@ -277,7 +277,7 @@ def test_batched_hyperedge_gemm():
     x = (rng.standard_normal((2,) * len(xl)) + 1j * rng.standard_normal((2,) * len(xl))) / 8
     y = (rng.standard_normal((2,) * len(yl)) + 1j * rng.standard_normal((2,) * len(yl))) / 8
     w = rng.standard_normal((2, 2)) + 0j
-    from paper_2002_01935_b200.tree import ContractionTree
+    from paper_2002_01935_b200.refpkg import ContractionTree
     tn = TensorNetwork([TensorNode(0, xl, x), TensorNode(1, yl, y), TensorNode(2, bl, w)], tab,
                        tuple(ml + nl))
     tree = ContractionTree((0, 1, 2), [(0, 1), (3, 2)])
@@ -331,7 +331,7 @@ def test_gemm_path_odd_dims(dims):
     x = (rng.standard_normal(xs) + 1j * rng.standard_normal(xs)) / np.sqrt(np.prod(xs) ** 0.5)
     y = (rng.standard_normal(ys) + 1j * rng.standard_normal(ys)) / np.sqrt(np.prod(ys) ** 0.5)
     w = rng.standard_normal(3) + 0j
-    from paper_2002_01935_b200.tree import ContractionTree
+    from paper_2002_01935_b200.refpkg import ContractionTree
     tn = TensorNetwork([TensorNode(0, xl, x), TensorNode(1, yl, y), TensorNode(2, ["b"], w)], tab,
                        tuple(nl[:2] + ml + nl[2:]))
     tree = ContractionTree((0, 1, 2), [(0, 1), (3, 2)])
@@ -349,8 +349,8 @@ def test_gemm_path_odd_dims(dims):
 
 
 def test_edge_cases_single_leaf_hyperedge_dim1():
-    from paper_2002_01935_b200.network import from_arrays
-    from paper_2002_01935_b200.tree import ContractionTree
+    from paper_2002_01935_b200.refpkg import from_arrays
+    from paper_2002_01935_b200.refpkg import ContractionTree
     rng = np.random.default_rng(11)
     # single-node network, output subset, sliced dangling label
     a = rng.standard_normal((2, 3, 4)) + 1j * rng.standard_normal((2, 3, 4))
@@ -375,8 +375,8 @@ def test_edge_cases_single_leaf_hyperedge_dim1():
 def test_sliced_label_without_carrier_multiplies_by_dim():
     """A sliced index carried by no tensor contributes a factor d (every slice
     is identical) -- same as the oracle's slice loop."""
-    from paper_2002_01935_b200.network import TensorNetwork, TensorNode
-    from paper_2002_01935_b200.tree import ContractionTree
+    from paper_2002_01935_b200.refpkg import TensorNetwork, TensorNode
+    from paper_2002_01935_b200.refpkg import ContractionTree
     rng = np.random.default_rng(2)
     x = rng.standard_normal((2, 2)) + 0j
     y = rng.standard_normal((2, 2)) + 0j
@@ -392,7 +392,7 @@ def test_large_sliced_leaves_gather():
     """Slice-dependent leaves of very different sizes in one gather launch
     (per-job block ranges), sliced labels between kept ones (no run merge
     across them) and mixed dims; every slice against the oracle."""
-    from paper_2002_01935_b200.tree import ContractionTree
+    from paper_2002_01935_b200.refpkg import ContractionTree
     rng = np.random.default_rng(5)
     tab = {"m0": 4, "s0": 2, "k0": 4, "m1": 4, "k1": 4, "m2": 512, "s1": 3, "n0": 8, "t": 2}
     shapes = {0: ["m0", "s0", "k0", "m1", "k1", "m2"], 1: ["k1", "s1", "k0", "n0"], 2: ["n0", "s1", "t"]}
@@ -473,7 +473,7 @@ def test_contract_sliced_device_list_sums_on_device(strip):
 def test_high_rank_sliced_leaf():
     """A rank-21 leaf carrying a sliced label (kept labels merge into two
     contiguous runs, so the gather's 16-run limit is not hit)."""
-    from paper_2002_01935_b200.tree import ContractionTree
+    from paper_2002_01935_b200.refpkg import ContractionTree
     rng = np.random.default_rng(11)
     al = [f"a{i}" for i in range(10)]
     bl = [f"b{i}" for i in range(10)]
@@ -494,7 +494,7 @@ def test_high_rank_sliced_leaf():
 def test_stacked_b_gemm_shapes(dims):
     """The stacked-B 2-CTA GEMM (M >= 1024 rows of A): batched hyperedge
     labels, N not a multiple of the 128-column tile, K padded to 16."""
-    from paper_2002_01935_b200.tree import ContractionTree
+    from paper_2002_01935_b200.refpkg import ContractionTree
     rng = np.random.default_rng(21)
     bl = [f"h{i}" for i in range(1)] if dims["b"] > 1 else []
     ml = [f"m{i}" for i in range(len(dims["m"]))]
@@ -522,7 +522,7 @@ def test_stacked_parent_fed_by_direct_children():
     """A stacked-B parent GEMM whose B operand planes (incl. the negated
     imaginary planes) are written by a child GEMM's epilogue, vs the
     materialised path and the oracle."""
-    from paper_2002_01935_b200.tree import ContractionTree
+    from paper_2002_01935_b200.refpkg import ContractionTree
     rng = np.random.default_rng(8)
     al = [f"a{i}" for i in range(11)]
     kl = [f"k{i}" for i in range(7)]

@@ -11,7 +11,7 @@ from _util import case_objects
 from paper_2002_01935_b200 import _native as nat
 from paper_2002_01935_b200.executor import SlicedPlan
 from paper_2002_01935_b200.slicing import sliced_metrics
-from paper_2002_01935_b200.tree import ContractionTree, metrics
+from paper_2002_01935_b200.refpkg import ContractionTree, metrics
 from paper_2002_01935_b200.harness import generators as gen
 
 
@@ -92,27 +92,30 @@ def test_vertex_kinds_and_hoisting():
     plan.close()
 
 
-def test_accepts_reference_objects_when_available():
-    """The executor is a drop-in for the reference's own objects."""
-    import sys
-    ref = "/root/reference/pkg/src"
-    import os
-    if not os.path.isdir(ref):
-        pytest.skip("reference not present (GPU box)")
-    sys.path.insert(0, ref)
-    try:
-        from hypertn import network as rnet, tree as rtree
-        from hypertn.drivers import greedy as rgreedy
-    finally:
-        sys.path.remove(ref)
-    tn0 = gen.random_regular(16, 3, seed=2)
-    rtn = rnet.TensorNetwork([rnet.TensorNode(n.id, n.indices, n.data) for n in tn0.nodes],
-                             dict(tn0.index_table), ())
-    rt = rgreedy.greedy_sample(rtn, 1.0, 0.0, 0)
-    plan = SlicedPlan(rtn, rt, list(rtn.index_table)[:2])
-    assert plan.ops_per_slice * plan.d == sliced_metrics(rt, rtn, list(rtn.index_table)[:2])[1]
-    assert plan.ops_per_slice * 1 <= rtree.metrics(rt, rtn).cost * 4
+def test_accepts_reference_objects():
+    """The executor plugs under the reference's own objects: hypertn
+    TensorNetwork + a greedy_sample tree (drivers/greedy.py:144)."""
+    from paper_2002_01935_b200 import refpkg
+    tn = gen.random_regular(16, 3, seed=2)
+    assert type(tn) is refpkg.network.TensorNetwork
+    rt = refpkg.greedy_sample(tn, 1.0, 0.0, 0)
+    assert type(rt) is refpkg.tree.ContractionTree
+    plan = SlicedPlan(tn, rt, list(tn.index_table)[:2])
+    assert plan.ops_per_slice * plan.d == sliced_metrics(rt, tn, list(tn.index_table)[:2])[1]
+    assert plan.ops_per_slice * 1 <= refpkg.metrics(rt, tn).cost * 4
     plan.close()
+
+
+def test_no_forked_reference_modules():
+    """The package carries no copy of the reference's data model / tree layer."""
+    import os
+    import paper_2002_01935_b200 as pkg
+    d = os.path.dirname(pkg.__file__)
+    assert not os.path.exists(os.path.join(d, "network.py"))
+    assert not os.path.exists(os.path.join(d, "tree.py"))
+    from paper_2002_01935_b200 import refpkg
+    assert refpkg.network.__file__.startswith(refpkg.REF_INSTALL) or \
+        refpkg.network.__file__.startswith(refpkg.REF_SOURCE)
 
 
 def test_auto_slice_fits_budget():

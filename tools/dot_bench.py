@@ -5,8 +5,8 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2002_01935_b200.executor import SlicedPlan
-from paper_2002_01935_b200.network import TensorNetwork, TensorNode
-from paper_2002_01935_b200.tree import ContractionTree
+from paper_2002_01935_b200.refpkg import TensorNetwork, TensorNode
+from paper_2002_01935_b200.refpkg import ContractionTree
 n_lab = 26
 labels = [f"a{i}" for i in range(n_lab)]
 rng = np.random.default_rng(0)

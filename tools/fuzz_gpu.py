@@ -20,9 +20,9 @@ import oracle
 from paper_2002_01935_b200.executor import SlicedPlan
 from paper_2002_01935_b200.harness import generators as gen
 from paper_2002_01935_b200.harness.paths import greedy_tree
-from paper_2002_01935_b200.network import TensorNode
+from paper_2002_01935_b200.refpkg import TensorNode
 from paper_2002_01935_b200.slicing import greedy_slice
-from paper_2002_01935_b200.tree import metrics
+from paper_2002_01935_b200.refpkg import metrics
 
 
 def make(seed):

@@ -5,8 +5,8 @@ import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2002_01935_b200.executor import SlicedPlan
-from paper_2002_01935_b200.network import TensorNetwork, TensorNode
-from paper_2002_01935_b200.tree import ContractionTree
+from paper_2002_01935_b200.refpkg import TensorNetwork, TensorNode
+from paper_2002_01935_b200.refpkg import ContractionTree
 kind = sys.argv[1] if len(sys.argv) > 1 else "random"
 rng = np.random.default_rng(0)
 ml = [f"m{i}" for i in range(13)]; nl = [f"n{i}" for i in range(13)]; kl = [f"k{i}" for i in range(12)]

@@ -4,7 +4,7 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2002_01935_b200.executor import SlicedPlan
-from paper_2002_01935_b200.network import TensorNetwork, TensorNode
+from paper_2002_01935_b200.refpkg import TensorNetwork, TensorNode
 # two-tensor network whose single vertex is a GEMM: x[m..,k..], y[n..,k..]
 def net(lm, ln, lk, seed):
     rng = np.random.default_rng(seed)
@@ -13,7 +13,7 @@ def net(lm, ln, lk, seed):
     x = (rng.standard_normal((2,)*(lm+lk)) + 1j*rng.standard_normal((2,)*(lm+lk)))
     y = (rng.standard_normal((2,)*(ln+lk)) + 1j*rng.standard_normal((2,)*(ln+lk)))
     return TensorNetwork([TensorNode(0, ml+kl, x), TensorNode(1, nl+kl, y)], tab, tuple(ml+nl))
-from paper_2002_01935_b200.tree import ContractionTree
+from paper_2002_01935_b200.refpkg import ContractionTree
 for (lm, ln, lk) in [(13, 13, 12), (12, 12, 14), (11, 11, 16)]:
     tn = net(lm, ln, lk, 0)
     tree = ContractionTree((0, 1), [(0, 1)])

@@ -5,8 +5,8 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 from paper_2002_01935_b200.executor import SlicedPlan
-from paper_2002_01935_b200.network import TensorNetwork, TensorNode
-from paper_2002_01935_b200.tree import ContractionTree
+from paper_2002_01935_b200.refpkg import TensorNetwork, TensorNode
+from paper_2002_01935_b200.refpkg import ContractionTree
 rng = np.random.default_rng(0)
 ml = [f"m{i}" for i in range(14)]
 kl = [f"k{i}" for i in range(13)]

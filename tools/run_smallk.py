@@ -6,8 +6,8 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 from paper_2002_01935_b200.executor import SlicedPlan
-from paper_2002_01935_b200.network import TensorNetwork, TensorNode
-from paper_2002_01935_b200.tree import ContractionTree
+from paper_2002_01935_b200.refpkg import TensorNetwork, TensorNode
+from paper_2002_01935_b200.refpkg import ContractionTree
 rng = np.random.default_rng(0)
 # optional label counts: run_smallk.py reps [n_a n_k n_b n_c]  (M = 2^n_a, K = 2^n_k, N = 2^n_b)
 na, nk, nb, nc = (int(x) for x in sys.argv[2:6]) if len(sys.argv) > 5 else (12, 3, 13, 8)
