@@ -233,6 +233,20 @@ def run_reference(args):
     return 0
 
 
+def spawn_ranks(n):
+    """`bench.py --gpus N` without a launcher: start one rank per GPU under
+    torch.distributed.run (127.0.0.1 rendezvous) and return its exit code.
+    Each child sees WORLD_SIZE and runs the per-rank path below."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 NOMINAL_TF32 = 1100.0  # TFLOP/s dense, B200 (context only)
 
 
@@ -256,6 +270,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
 
     import numpy as np
     import torch
@@ -264,6 +280,9 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; reporting the {world} ranks that run",
+              file=sys.stderr)
     # TNX_BENCH_BACKEND=gloo lets the multi-rank logic be exercised with
     # several ranks sharing one GPU (no kernel waits on another rank); the
     # production path is NCCL with one GPU per rank.

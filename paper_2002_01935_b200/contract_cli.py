@@ -36,7 +36,7 @@ def main(argv=None):
     from .refpkg import DataError, load_network
     from .refpkg import tree_from_path_dict
     from .slicing import SliceSet, greedy_slice
-    from .executor import SlicedPlan, _finish
+    from .executor import SlicedPlan, _finish, _combine_exp
 
     ap = argparse.ArgumentParser(prog="contract")
     ap.add_argument("network")
@@ -44,7 +44,7 @@ def main(argv=None):
     ap.add_argument("--slices")
     ap.add_argument("--target-width", type=float)
     ap.add_argument("--slice-range", type=int, nargs=2)
-    ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "fp32"])
+    ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "fp32", "tf32-bf16x"])
     ap.add_argument("--strip-exponent", action="store_true")
     ap.add_argument("--device", type=int, default=0)
     try:
@@ -68,17 +68,41 @@ def main(argv=None):
     except (ValueError, OSError, json.JSONDecodeError) as exc:
         print(json.dumps({"error": str(exc)}), file=sys.stderr)
         return 2
-    plan = SlicedPlan(tn, tree, ss, device=args.device, precision=args.precision)
+
+    def err(code, exc):
+        print(json.dumps({"error": str(exc)}), file=sys.stderr)
+        return code
+
+    try:
+        # strip_exponent: every intermediate is renormalised on the
+        # device, so networks whose value overflows complex64/128 still contract
+        plan = SlicedPlan(tn, tree, ss, device=args.device, precision=args.precision,
+                          strip_exponent=args.strip_exponent)
+    except DataError as exc:
+        return err(4, exc)
+    except ValueError as exc:
+        return err(2, exc)
+    except MemoryError as exc:
+        return err(5, exc)
     try:
         s0, s1 = args.slice_range if args.slice_range else (0, plan.d)
+        if not 0 <= s0 <= s1 <= plan.d:
+            return err(2, ValueError(f"--slice-range [{s0}, {s1}) out of [0, {plan.d})"))
         plan.bind()
         plan.run(s0, s1)
-        try:
-            val, e10 = _finish(plan.result(), tn, args.strip_exponent)
-        except FloatingPointError as exc:
-            print(json.dumps({"error": str(exc)}), file=sys.stderr)
-            return 5
+        if args.strip_exponent:
+            val, e10 = _combine_exp([plan.result_exp()], tn)
+        else:
+            val, e10 = _finish(plan.result(), tn, False)
         doc = result_document(val, e10, plan.ops_per_slice * (s1 - s0), plan.stats(), s1 - s0)
+    except FloatingPointError as exc:
+        return err(5, exc)
+    except DataError as exc:
+        return err(4, exc)
+    except ValueError as exc:
+        return err(2, exc)
+    except (MemoryError, RuntimeError) as exc:
+        return err(5, exc)
     finally:
         plan.close()
     print(json.dumps(doc))

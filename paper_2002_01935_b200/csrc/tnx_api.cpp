@@ -206,9 +206,18 @@ struct Plan {
   std::vector<GemmPlan> gemms;
   AccumParams accum{};
   float2* staging = nullptr;       // pinned host staging for complex128 leaf uploads
+  // cross-stream ordering: every call that enqueues work records `order_ev` on
+  // its stream; a later call on another stream waits on it first (bind / run /
+  // reset / result share the arena, the accumulator and the staging buffer)
+  cudaEvent_t order_ev = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool order_valid = false;
 
   ~Plan() { release(); }
   void release() {
+    if (order_ev) cudaEventDestroy(order_ev);
+    order_ev = nullptr;
+    order_valid = false;
     if (gexec) cudaGraphExecDestroy(gexec);
     if (graph) cudaGraphDestroy(graph);
     if (hgexec) cudaGraphExecDestroy(hgexec);
@@ -1207,6 +1216,21 @@ void build_tables(Plan& P) {
 
 }  // namespace
 
+// Order stream `st` after the plan's previous work (if it ran on another stream).
+static int order_after(Plan& P, cudaStream_t st) {
+  if (P.order_valid && P.last_stream != st) TNX_CUDA(cudaStreamWaitEvent(st, P.order_ev, 0));
+  return TNX_OK;
+}
+
+// Record the end of this call's work on `st` for the next call to order after.
+static int mark_done(Plan& P, cudaStream_t st) {
+  if (!P.order_ev) TNX_CUDA(cudaEventCreateWithFlags(&P.order_ev, cudaEventDisableTiming));
+  TNX_CUDA(cudaEventRecord(P.order_ev, st));
+  P.last_stream = st;
+  P.order_valid = true;
+  return TNX_OK;
+}
+
 extern "C" {
 
 const char* tnx_last_error(void) { return g_err.c_str(); }
@@ -1352,6 +1376,7 @@ int tnx_bind_leaves(void* plan, const void* const* leaf_data, int32_t dtype, int
     P.bound = true;
   }
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.own;
+  if (int orc = order_after(P, st)) return orc;
   // upload leaves
   int64_t max_leaf = 0;
   for (int i = 0; i < P.n; ++i) max_leaf = std::max<int64_t>(max_leaf, P.prod(P.leaf_labels[i]));
@@ -1361,7 +1386,9 @@ int tnx_bind_leaves(void* plan, const void* const* leaf_data, int32_t dtype, int
         TNX_CUDA(cudaMallocHost(&P.staging, P.pool_elems * 8));
         std::memset(P.staging, 0, P.pool_elems * 8);
       }
-      TNX_CUDA(cudaStreamSynchronize(st));  // previous upload finished reading the staging buffer
+      // the previous upload (on whichever stream) finished reading the staging buffer
+      TNX_CUDA(cudaStreamSynchronize(st));
+      if (P.order_valid) TNX_CUDA(cudaEventSynchronize(P.order_ev));
       for (int i = 0; i < P.n; ++i) {
         const double* src = static_cast<const double*>(leaf_data[i]);
         int64_t sz = P.prod(P.leaf_labels[i]);
@@ -1426,7 +1453,7 @@ int tnx_bind_leaves(void* plan, const void* const* leaf_data, int32_t dtype, int
     P.graph = g;
     TNX_CUDA(cudaGraphInstantiate(&P.gexec, g, 0));
   }
-  return TNX_OK;
+  return mark_done(P, st);
 }
 
 int tnx_run_slices(void* plan, uint64_t s_begin, uint64_t s_end, void* stream) {
@@ -1437,6 +1464,7 @@ int tnx_run_slices(void* plan, uint64_t s_begin, uint64_t s_end, void* stream) {
   TNX_CUDA(cudaSetDevice(P.device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.own;
   if (s_begin == s_end) return TNX_OK;
+  if (int orc = order_after(P, st)) return orc;
   cudaError_t e = launch_set_counter(P.counter, s_begin, st);
   if (e != cudaSuccess) return fail(TNX_ERR_CUDA, cudaGetErrorString(e));
   for (uint64_t s = s_begin; s < s_end; ++s) {
@@ -1447,17 +1475,18 @@ int tnx_run_slices(void* plan, uint64_t s_begin, uint64_t s_end, void* stream) {
       if (rc) return rc;
     }
   }
-  return TNX_OK;
+  return mark_done(P, st);
 }
 
 int tnx_reset_accumulator(void* plan, void* stream) {
   Plan& P = *static_cast<Plan*>(plan);
   if (!P.bound) return fail(TNX_ERR_STATE, "not bound");
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.own;
+  if (int orc = order_after(P, st)) return orc;
   TNX_CUDA(cudaMemsetAsync(P.acc, 0, std::max<int64_t>(P.out_size, 1) * 16, st));
   TNX_CUDA(cudaMemsetAsync(P.comp, 0, std::max<int64_t>(P.out_size, 1) * 16, st));
   if (P.d_acc_exp) TNX_CUDA(cudaMemsetAsync(P.d_acc_exp, 0, std::max<int64_t>(P.out_size, 1) * 8, st));
-  return TNX_OK;
+  return mark_done(P, st);
 }
 
 int tnx_partial_result(void* plan, double* out, int64_t out_elems, void* stream) {
@@ -1465,6 +1494,7 @@ int tnx_partial_result(void* plan, double* out, int64_t out_elems, void* stream)
   if (!P.bound) return fail(TNX_ERR_STATE, "not bound");
   if (out_elems != P.out_size) return fail(TNX_ERR_INVALID, "output size mismatch");
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.own;
+  if (int orc = order_after(P, st)) return orc;
   TNX_CUDA(cudaMemcpyAsync(out, P.acc, P.out_size * 16, cudaMemcpyDeviceToHost, st));
   TNX_CUDA(cudaStreamSynchronize(st));
   return TNX_OK;
@@ -1476,6 +1506,7 @@ int tnx_partial_result_exp(void* plan, double* out, int64_t* exp2, int64_t out_e
   if (!P.strip()) return fail(TNX_ERR_STATE, "plan was not created with TNX_FLAG_STRIP_EXPONENT");
   if (out_elems != P.out_size) return fail(TNX_ERR_INVALID, "output size mismatch");
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.own;
+  if (int orc = order_after(P, st)) return orc;
   TNX_CUDA(cudaMemcpyAsync(out, P.acc, P.out_size * 16, cudaMemcpyDeviceToHost, st));
   TNX_CUDA(cudaMemcpyAsync(exp2, P.d_acc_exp, P.out_size * 8, cudaMemcpyDeviceToHost, st));
   TNX_CUDA(cudaStreamSynchronize(st));
@@ -1537,6 +1568,8 @@ int tnx_allreduce(void* const* plans, int32_t nplans, void* const* streams) {
   for (int i = 0; i < n && e == cudaSuccess; ++i) {
     Plan& P = *static_cast<Plan*>(plans[i]);
     e = cudaSetDevice(P.device);
+    if (e == cudaSuccess && P.order_valid && P.last_stream != stream_of(i))
+      e = cudaStreamWaitEvent(stream_of(i), P.order_ev, 0);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&evs[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventRecord(evs[i], stream_of(i));
     if (e == cudaSuccess) e = cudaSetDevice(R.device);
@@ -1561,6 +1594,17 @@ int tnx_allreduce(void* const* plans, int32_t nplans, void* const* streams) {
   for (int i = 1; i < n && e == cudaSuccess; ++i) {
     e = cudaSetDevice(static_cast<Plan*>(plans[i])->device);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(stream_of(i), evs[0], 0);
+  }
+  // later calls on other streams order after the exchange
+  for (int i = 0; i < n && e == cudaSuccess; ++i) {
+    Plan& P = *static_cast<Plan*>(plans[i]);
+    e = cudaSetDevice(P.device);
+    if (e == cudaSuccess && !P.order_ev) e = cudaEventCreateWithFlags(&P.order_ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(P.order_ev, stream_of(i));
+    if (e == cudaSuccess) {
+      P.last_stream = stream_of(i);
+      P.order_valid = true;
+    }
   }
   // events may be destroyed once recorded/waited on (resources are released on completion)
   cleanup();
@@ -1640,6 +1684,7 @@ int tnx_debug_vertex(void* plan, uint64_t s, int32_t v, float* out_c64, int64_t 
   if (out_elems != t.size) return fail(TNX_ERR_INVALID, "size mismatch: need " + std::to_string(t.size));
   TNX_CUDA(cudaSetDevice(P.device));
   cudaStream_t st = P.own;
+  if (int orc = order_after(P, st)) return orc;
   TNX_CUDA(cudaStreamSynchronize(st));
   const Vertex& vx = P.V[v - P.n];
   int rc;
@@ -1652,6 +1697,7 @@ int tnx_debug_vertex(void* plan, uint64_t s, int32_t v, float* out_c64, int64_t 
   }
   if (rc) return rc;
   TNX_CUDA(cudaMemcpyAsync(out_c64, P.ptr(t), t.size * 8, cudaMemcpyDeviceToHost, st));
+  if (int mrc = mark_done(P, st)) return mrc;
   TNX_CUDA(cudaStreamSynchronize(st));
   for (size_t i = 0; i < t.labels.size(); ++i) layout_labels[i] = t.labels[i];
   *rank_out = (int)t.labels.size();
@@ -1665,6 +1711,7 @@ int tnx_profile_slice(void* plan, uint64_t s, int32_t* types, int32_t* vertices,
   if ((u128)s >= P.d) return fail(TNX_ERR_INVALID, "slice out of range");
   TNX_CUDA(cudaSetDevice(P.device));
   cudaStream_t st = P.own;
+  if (int orc = order_after(P, st)) return orc;
   const int n = (int)P.slice_launches.size();
   std::vector<cudaEvent_t> ev(n + 1);
   for (auto& e : ev) TNX_CUDA(cudaEventCreate(&e));
@@ -1681,6 +1728,7 @@ int tnx_profile_slice(void* plan, uint64_t s, int32_t* types, int32_t* vertices,
     TNX_CUDA(cudaEventRecord(ev[i + 1], st));
     done = i + 1;
   }
+  if (int mrc = mark_done(P, st)) return mrc;
   TNX_CUDA(cudaStreamSynchronize(st));
   int m = std::min(done, (int)max_launches);
   for (int i = 0; i < m; ++i) {

@@ -162,7 +162,10 @@ class SlicedPlan:
     def bind(self, tn=None, stream=None, leaf_arrays=None):
         """Upload leaf data (host complex128 from ``tn`` nodes, or a list of
         contiguous complex64/complex128 host arrays / CUDA torch tensors in
-        SSA leaf order)."""
+        SSA leaf order).  Every array must hold exactly the leaf's
+        prod(dims) elements; a wrong size or dtype raises ``DataError``.
+        CUDA tensors are read on torch's current stream of the plan's device
+        unless ``stream`` is given."""
         tn = self.tn if tn is None else tn
         if leaf_arrays is None:
             arrs = []
@@ -172,22 +175,51 @@ class SlicedPlan:
                     raise ValueError(f"contract needs dense data on every node (node {nid})")
                 arrs.append(np.ascontiguousarray(nd.data, dtype=np.complex128))
             leaf_arrays = arrs
+        if len(leaf_arrays) != self.tree.n:
+            raise DataError(f"{len(leaf_arrays)} leaf arrays for {self.tree.n} leaves")
         loc, dtype, ptrs, hold = self._leaf_pointers(leaf_arrays)
+        if loc == nat.LOC_DEVICE and stream is None:
+            import torch
+            stream = torch.cuda.current_stream(self.device)
         self._hold = hold
         nat.check(self._lib.tnx_bind_leaves(self._h, ptrs, dtype, loc, self._stream(stream)))
         self._bound = True
         return self
 
+    def _leaf_sizes(self):
+        sizes = getattr(self, "_sizes", None)
+        if sizes is None:
+            sizes = []
+            for nid in self.tree.leaves:
+                p = 1
+                for lbl in self.tn.node(nid).indices:
+                    p *= self.tn.index_table[lbl]
+                sizes.append(p)
+            self._sizes = sizes
+        return sizes
+
     def _leaf_pointers(self, arrays):
         ptrs = (C.c_void_p * max(1, len(arrays)))()
+        sizes = self._leaf_sizes()
         first = arrays[0]
         if hasattr(first, "is_cuda") and first.is_cuda:
             import torch
             dt = first.dtype
-            dtype = nat.DTYPE_C64 if dt == torch.complex64 else nat.DTYPE_C128
+            if dt not in (torch.complex64, torch.complex128):
+                raise DataError(f"leaf tensors must be complex64 or complex128, got {dt}")
+            hold = []
             for i, a in enumerate(arrays):
-                ptrs[i] = a.contiguous().data_ptr()
-            return nat.LOC_DEVICE, dtype, ptrs, arrays
+                if not getattr(a, "is_cuda", False) or a.dtype != dt:
+                    raise DataError(f"leaf {i}: all leaf tensors must be CUDA tensors of dtype {dt}")
+                if a.device.index != self.device:
+                    raise DataError(f"leaf {i} lives on cuda:{a.device.index}, plan on cuda:{self.device}")
+                if a.numel() != sizes[i]:
+                    raise DataError(f"leaf {i}: {a.numel()} elements, its labels need {sizes[i]}")
+                c = a.contiguous()       # kept alive in `hold` until the next bind
+                hold.append(c)
+                ptrs[i] = c.data_ptr()
+            dtype = nat.DTYPE_C64 if dt == torch.complex64 else nat.DTYPE_C128
+            return nat.LOC_DEVICE, dtype, ptrs, hold
         # re-binding the same (contiguous, right-dtype) host arrays -- new values in
         # the same buffers, e.g. one bind per bitstring or per step -- reuses the
         # marshalled pointer table; the library still copies the data every bind
@@ -196,11 +228,16 @@ class SlicedPlan:
                 and all(a is b for a, b in zip(arrays, cache[0]))):
             return nat.LOC_HOST, cache[1], cache[2], cache[3]
         conv = []
-        dtype = nat.DTYPE_C64 if np.asarray(first).dtype == np.complex64 else nat.DTYPE_C128
+        first = np.asarray(first)
+        if not np.issubdtype(first.dtype, np.number):
+            raise DataError(f"leaf arrays must be numeric, got {first.dtype}")
+        dtype = nat.DTYPE_C64 if first.dtype == np.complex64 else nat.DTYPE_C128
         want = np.complex64 if dtype == nat.DTYPE_C64 else np.complex128
         reusable = True
         for i, a in enumerate(arrays):
             c = np.ascontiguousarray(a, dtype=want)
+            if c.size != sizes[i]:
+                raise DataError(f"leaf {i}: {c.size} elements, its labels need {sizes[i]}")
             reusable = reusable and c is a
             conv.append(c)
             ptrs[i] = c.__array_interface__["data"][0]
@@ -337,15 +374,45 @@ def _finish(val, tn, strip_exponent):
     return arr, exp10
 
 
-def _slice_range(d, slice_ids):
+def _slice_runs(d, slice_ids):
+    """Slice ids to run, as contiguous [a, b) runs in the given order.
+
+    ``None`` = every slice; a ``range`` with step 1 = one run; any other
+    iterable is a list of slice ids (the oracle's meaning, duplicates summed
+    twice), grouped into maximal consecutive runs."""
     if slice_ids is None:
-        return 0, d
+        return [(0, d)]
     if isinstance(slice_ids, range):
         if slice_ids.step != 1:
-            raise ValueError("slice_ids must be a contiguous range")
-        return slice_ids.start, slice_ids.stop
-    s0, s1 = slice_ids
-    return int(s0), int(s1)
+            raise ValueError("a slice_ids range must have step 1 (pass a list for other id sets)")
+        if not 0 <= slice_ids.start <= slice_ids.stop <= d:
+            raise ValueError(f"slice range [{slice_ids.start}, {slice_ids.stop}) out of [0, {d})")
+        return [(slice_ids.start, slice_ids.stop)] if slice_ids.stop > slice_ids.start else []
+    runs = []
+    for s in slice_ids:
+        s = int(s)
+        if not 0 <= s < d:
+            raise ValueError(f"slice id {s} out of [0, {d})")
+        if runs and runs[-1][1] == s:
+            runs[-1][1] = s + 1
+        else:
+            runs.append([s, s + 1])
+    return [(a, b) for a, b in runs]
+
+
+def _split_runs(runs, G):
+    """Split runs into G consecutive shares of (nearly) equal slice counts."""
+    total = sum(b - a for a, b in runs)
+    cuts = [total * g // G for g in range(G + 1)]
+    shares = [[] for _ in range(G)]
+    pos = 0
+    for a, b in runs:
+        for g in range(G):
+            lo, hi = max(a, a + cuts[g] - pos), min(b, a + cuts[g + 1] - pos)
+            if hi > lo:
+                shares[g].append((lo, hi))
+        pos += b - a
+    return shares
 
 
 def allreduce_plans(plans, streams=None):
@@ -368,9 +435,10 @@ def contract_sliced(tn, tree, slice_set=(), options=None, *, slice_ids=None, dev
     """Sum over slice assignments of the per-slice contraction.
 
     Returns (value-or-open-tensor, exponent10, op_count) with op_count the
-    exact MAC count executed (C_s for the full range).  ``devices`` splits
-    the slice range into contiguous per-device blocks (one host thread per
-    device) and sums the complex128 partials.
+    exact MAC count executed (C_s for the full range).  ``slice_ids``
+    restricts the sum: a step-1 ``range`` or a list of slice ids (see
+    ``_slice_runs``).  ``devices`` splits the ids into contiguous per-device
+    shares (one host thread per device) and sums the complex128 partials.
     """
     options = dict(options or {})
     strip = bool(options.get("strip_exponent", False))
@@ -379,18 +447,17 @@ def contract_sliced(tn, tree, slice_set=(), options=None, *, slice_ids=None, dev
                         strip_exponent=strip)
              for d in devices]
     try:
-        s0, s1 = _slice_range(plans[0].d, slice_ids)
-        if not 0 <= s0 <= s1 <= plans[0].d:
-            raise ValueError("slice range out of [0, d)")
+        runs = _slice_runs(plans[0].d, slice_ids)
         G = len(plans)
-        bounds = [s0 + (s1 - s0) * g // G for g in range(G + 1)]
+        shares = _split_runs(runs, G)
         errs = [None] * G
 
         def work(g):
             try:
                 p = plans[g]
                 p.bind()
-                p.run(bounds[g], bounds[g + 1])
+                for a, b in shares[g]:
+                    p.run(a, b)
             except BaseException as exc:  # noqa: BLE001
                 errs[g] = exc
 
@@ -407,7 +474,7 @@ def contract_sliced(tn, tree, slice_set=(), options=None, *, slice_ids=None, dev
                 raise e
         if G > 1:
             allreduce_plans(plans)
-        ops = plans[0].ops_per_slice * (s1 - s0)
+        ops = plans[0].ops_per_slice * sum(b - a for a, b in runs)
         if strip:
             val, exp10 = _combine_exp([plans[0].result_exp()], tn)
             return val, exp10, ops
@@ -462,15 +529,42 @@ def _open_pattern(bitstring):
     return tuple(i for i, b in enumerate(bitstring) if b in _OPEN)
 
 
+def _default_tree(tn, trials=4, seed=0):
+    """Tree for ``amplitude`` when the caller gives none: the reference's own
+    Boltzmann-greedy driver (``greedy_sample``, drivers/greedy.py:144-158),
+    best of ``trials`` (alpha, tau) shots by (cost, width) -- path finding stays
+    the reference's (north_star)."""
+    from .refpkg import greedy_sample, metrics
+    rng = np.random.default_rng(seed)
+    best, best_key = None, None
+    for t in range(max(1, trials)):
+        alpha, tau = (1.0, 0.0) if t == 0 else (float(rng.uniform(0.0, 2.0)), float(rng.choice([0.0, 0.05])))
+        tree = greedy_sample(tn, alpha, tau, seed + t)
+        m = metrics(tree, tn)
+        key = (m.cost, m.width)
+        if best is None or key < best_key:
+            best, best_key = tree, key
+    return best
+
+
+def _device_free_bytes(device):
+    import torch
+    free, _total = torch.cuda.mem_get_info(device)
+    return free
+
+
 class AmplitudeEngine:
     """One compiled plan reused across bitstrings (only leaf data changes,
     PAPER.md:530).  ``open_qubits`` (positions, or a pattern
     string with 'x' marks) selects legs left open: every call must then mark
-    exactly those positions and returns the (2,)*N_f amplitude tensor."""
+    exactly those positions and returns the (2,)*N_f amplitude tensor.
 
-    def __init__(self, circuit_tn, tree, slice_set=(), device=0, precision=None, open_qubits=()):
+    ``tree=None`` takes the reference's ``greedy_sample`` tree of the
+    projected network; ``slice_set=None`` slices it to the largest W_s whose
+    plan fits the device (``auto_slice``)."""
+
+    def __init__(self, circuit_tn, tree=None, slice_set=(), device=0, precision=None, open_qubits=()):
         self.tn = circuit_tn
-        self.tree = tree
         if isinstance(open_qubits, str):
             open_qubits = _open_pattern(open_qubits)
         self.open = tuple(sorted(int(i) for i in open_qubits))
@@ -478,25 +572,42 @@ class AmplitudeEngine:
         if any(not 0 <= i < n for i in self.open):
             raise ValueError(f"open qubit positions {self.open} out of range for {n} legs")
         base = "".join("x" if i in self.open else "0" for i in range(n))
-        self.plan = SlicedPlan(_project(circuit_tn, base), tree, slice_set, device=device, precision=precision)
+        ptn = _project(circuit_tn, base)
+        self.tree = _default_tree(ptn) if tree is None else tree
+        if slice_set is None:
+            from .slicing import auto_slice
+            slice_set, _ = auto_slice(self.tree, ptn, _device_free_bytes(device), precision=_precision(precision))
+        self.slice_set = slice_set
+        self.plan = SlicedPlan(ptn, self.tree, slice_set, device=device, precision=precision)
 
     def __call__(self, bitstring):
+        """c_x (or the open-qubit tensor), including the network's
+        ``10**norm_exponent`` factor (network.py:55-58)."""
         if _open_pattern(bitstring) != self.open:
             raise ValueError(f"open positions of {bitstring!r} differ from the engine's {self.open}")
         ptn = _project(self.tn, bitstring)
         self.plan.bind(ptn)
         self.plan.run()
-        val, _ = _finish(self.plan.result(), ptn, False)
+        val, exp10 = _finish(self.plan.result(), ptn, False)
+        if exp10:
+            val = val * 10.0 ** exp10
+            if not np.all(np.isfinite(np.asarray(val))):
+                raise FloatingPointError("amplitude overflows complex128 after applying norm_exponent")
         return val
 
     def close(self):
         self.plan.close()
 
 
-def amplitude(circuit_tn, bitstring, tree, slice_set=(), **kw):
+def amplitude(circuit_tn, bitstring, tree=None, slice_set=None, **kw):
     """c_x = <x| U |0> of a circuit network whose open legs are the qubits
-    (SPEC.md:533); 'x' / '*' in the bitstring leave that qubit open and return
-    the amplitude tensor over the open qubits."""
+    (``amplitude(circuit_tn, bitstring) -> complex``).  The tree
+    defaults to the reference's ``greedy_sample`` on the projected network and
+    the slicing to the largest W_s that fits the device; 'x' / '*' in the
+    bitstring leave that qubit open and return the amplitude tensor over the
+    open qubits."""
+    if len(bitstring) != len(circuit_tn.output):
+        raise ValueError(f"bitstring length {len(bitstring)} != {len(circuit_tn.output)} open legs")
     eng = AmplitudeEngine(circuit_tn, tree, slice_set, open_qubits=_open_pattern(bitstring), **kw)
     try:
         return eng(bitstring)

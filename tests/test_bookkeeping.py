@@ -172,3 +172,22 @@ def test_amplitude_projection_open_markers():
         _project(tn, "x1")
     with pytest.raises(ValueError):
         _project(tn, "a10")
+
+
+def test_slice_runs_and_device_shares():
+    from paper_2002_01935_b200.executor import _slice_runs, _split_runs
+    assert _slice_runs(16, None) == [(0, 16)]
+    assert _slice_runs(16, range(3, 9)) == [(3, 9)]
+    assert _slice_runs(16, [0, 7]) == [(0, 1), (7, 8)]
+    assert _slice_runs(16, [4, 5, 6, 1, 2]) == [(4, 7), (1, 3)]
+    with pytest.raises(ValueError):
+        _slice_runs(16, [16])
+    with pytest.raises(ValueError):
+        _slice_runs(16, range(0, 8, 2))
+    runs = [(0, 5), (10, 13)]
+    for G in (1, 2, 3, 8):
+        shares = _split_runs(runs, G)
+        flat = [s for sh in shares for a, b in sh for s in range(a, b)]
+        assert flat == list(range(0, 5)) + list(range(10, 13))
+        sizes = [sum(b - a for a, b in sh) for sh in shares]
+        assert max(sizes) - min(sizes) <= 1

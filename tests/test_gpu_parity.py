@@ -50,7 +50,7 @@ def test_golden_values(case, precision):
         assert ops == int(ent["Cs"])
         check_close(val, arr_from_json(ent["value"]), tn, tree, S)
         for sid, v in ent.get("per_slice", {}).items():
-            got, _, _ = contract_sliced(tn, tree, S, slice_ids=(int(sid), int(sid) + 1),
+            got, _, _ = contract_sliced(tn, tree, S, slice_ids=range(int(sid), int(sid) + 1),
                                         precision=precision)
             check_close(got, arr_from_json(v), tn, tree, S)
 
