@@ -35,6 +35,7 @@ CONFIGS = {
     "cfg4_7x7_d40": (lambda: gen.grid_circuit(7, 7, 40, seed=0), 48, False),
     "cfg4p_7x7_d16": (lambda: gen.grid_circuit(7, 7, 16, seed=0), 48, True),
     "cfg4p_7x7_d20": (lambda: gen.grid_circuit(7, 7, 20, seed=0), 48, True),
+    "cfg4p_7x7_d24": (lambda: gen.grid_circuit(7, 7, 24, seed=0), 48, True),
     "cfg5_syc53_m12": (lambda: gen.sycamore_circuit(12, seed=0), 48, False),
     # diagonal-reduced (hyperedge) forms of the cfg4 circuits
     "cfg4d_7x7_d40_diag": (lambda: gen.grid_circuit(7, 7, 40, seed=0, diag=True), 48, False),

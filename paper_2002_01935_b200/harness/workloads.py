@@ -35,6 +35,8 @@ CONFIGS = {
                           desc="7x7 (1+16+1) circuit amplitude (parity companion of cfg4)"),
     "cfg4p_7x7_d20": dict(make=lambda: gen.grid_circuit(7, 7, 20, seed=0), ws=21,
                           desc="7x7 (1+20+1) circuit amplitude (parity companion of cfg4)"),
+    "cfg4p_7x7_d24": dict(make=lambda: gen.grid_circuit(7, 7, 24, seed=0), ws=27,
+                          desc="7x7 (1+24+1) circuit amplitude (parity companion of cfg4; oracle sliced at W_s=27)"),
     "cfg5_syc53_m12": dict(make=lambda: gen.sycamore_circuit(12, seed=0), ws=27,
                            desc="Sycamore-like 53-qubit m=12 circuit amplitude, synthetic fSim"),
     # the cfg4 circuit diagonal-reduced (CZ and T gates as hyperedge nodes,
