@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -112,26 +113,14 @@ def load_traffic():
     return None
 
 
-def measure_tf32_peak(torch):
-    """Dense TF32 tensor-core peak of this GPU, measured with cuBLAS."""
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = True
-    try:
-        n = 8192
-        a = torch.randn(n, n, device="cuda")
-        b = torch.randn(n, n, device="cuda")
-        best = 0.0
-        for _ in range(6):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            torch.matmul(a, b)
-            e1.record()
-            torch.cuda.synchronize()
-            best = max(best, 2 * n ** 3 / (e0.elapsed_time(e1) / 1e3) / 1e12)
-        del a, b
-        return best
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
+def load_mma_peak():
+    """Committed MMA-only ceiling (tools/mma_peak.py output), if present."""
+    for name in ("r02_mma_peak.json",):
+        path = os.path.join(REPO, "profiles", name)
+        if os.path.exists(path):
+            with open(path) as fh:
+                return json.load(fh), f"profiles/{name}"
+    return None, None
 
 
 def workload(args):
@@ -263,7 +252,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=90.0)
     ap.add_argument("--profile-out", default=None)
-    ap.add_argument("--no-tf32-probe", action="store_true")
+    ap.add_argument("--no-tf32-probe", action="store_true", help="skip the live MMA-only ceiling probe")
+    ap.add_argument("--sustained-s", type=float, default=10.0,
+                    help="after the headline, time ~this many seconds of further slices (0: skip)")
     ap.add_argument("--no-direct", action="store_true", help="disable GEMM->GEMM operand-plane fusion")
     ap.add_argument("--force-dist", action="store_true",
                     help="initialise torch.distributed even at world size 1 (exercises the NCCL path)")
@@ -354,6 +345,21 @@ def main():
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     ms_max = float(t_max.item())
 
+    def slice_values(ids):
+        """Per-slice values of `ids` (each contracted alone, not accumulated)."""
+        vals = []
+        for s_ in ids:
+            plan.reset(stream)
+            plan.run(s_, s_ + 1, stream)
+            vals.append(complex(np.asarray(plan.result(stream)).ravel()[0]))
+        return vals
+
+    def zero_fraction(vals):
+        """Slices whose value is zero in exact arithmetic: |v| below 1e-8 of the
+        largest |v| of the sample (they come out at ~1e-16 of it, noise)."""
+        big = max((abs(v) for v in vals), default=0.0)
+        return sum(1 for v in vals if abs(v) <= 1e-8 * big) / len(vals) if vals and big > 0 else None
+
     # final exchange: one all-reduce of the complex128 partial sums
     part = plan.result(stream)
     a0 = time.perf_counter()
@@ -364,6 +370,38 @@ def main():
     total_slices = K * world
     value = total_slices * flops_slice / (ms_max / 1e3) / 1e12
     slices_per_s = total_slices / (ms_max / 1e3)
+    timed_zero = zero_fraction(slice_values(range(base + W, base + W + K))) if st["out_elements"] == 1 else None
+
+    # sustained: the same per-slice work for >= --sustained-s seconds (the GEMMs
+    # run into the 1 kW power cap; the headline above is a ~0.5 s burst)
+    sustained = None
+    if args.sustained_s > 0:
+        n_s = max(K, int(math.ceil(args.sustained_s * 1e3 / (ms_max / K))))
+        s_base = world * (W + K) + rank * n_s
+        if s_base + n_s <= plan.d:
+            plan.reset(stream)
+            clk2 = ClockSampler(local).start()
+            barrier()
+            torch.cuda.synchronize()
+            f0 = torch.cuda.Event(enable_timing=True)
+            f1 = torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
+            plan.run(s_base, s_base + n_s, stream)
+            f1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            clocks2 = clk2.stop()
+            ms2 = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=red_dev)
+            if use_dist:
+                dist.all_reduce(ms2, op=dist.ReduceOp.MAX)
+            ms2 = float(ms2.item())
+            sample = list(range(s_base, s_base + n_s, max(1, n_s // 48)))
+            sustained = {"value": n_s * world * flops_slice / (ms2 / 1e3) / 1e12, "unit": "TFLOP/s",
+                         "seconds": ms2 / 1e3, "slices_per_rank": n_s, "ms_per_step": ms2 / n_s,
+                         "slices_per_s": n_s * world / (ms2 / 1e3), "clocks": clocks2,
+                         "zero_slice_fraction": zero_fraction(slice_values(sample))
+                         if st["out_elements"] == 1 else None,
+                         "zero_sample": f"{len(sample)} slices spread over the sustained range"}
 
     # per-launch profile of one slice (CUDA events on the launching stream)
     prof_b = plan.profile_slice(base + W, with_bytes=True)
@@ -374,13 +412,35 @@ def main():
     n_gemm = sum(1 for k, v, t in prof if k == "gemm")
     slice_ms = sum(t for _, _, t in prof)
     peaks, peak_kind = load_peaks()
-    p_tf32 = measure_tf32_peak(torch) if not args.no_tf32_probe else None
-    # primary roofline: the driver-measured bf16 peak -> TF32 (half rate) -> /3 split passes
-    p_c = peaks["bf16_tflops"] / 2.0 / 3.0
-    peak_src = (f"{peak_kind} MEASURED_PEAKS bf16_tflops {peaks['bf16_tflops']} / 2 (TF32 = half the "
-                f"BF16 tensor rate) / 3 (split-TF32 passes)")
-    if p_tf32:
-        peak_src += f"; live cuBLAS TF32 8192^3 this run: {p_tf32:.1f} TFLOP/s (/3 = {p_tf32 / 3:.1f})"
+    # Roofline denominator: the tensor pipe's own ceiling, measured live by an
+    # MMA-only tcgen05.mma kind::tf32 loop (tnx_mma_peak: no TMA, no epilogue,
+    # operands resident in shared memory, one CTA pair per SM pair), divided
+    # by 3 (split-TF32: 24 M N K real tensor flop per 8 M N K complex flop).
+    from paper_2002_01935_b200 import _native
+    probe = None
+    if not args.no_tf32_probe:
+        best = None
+        for cg in (2, 1):
+            _native.mma_peak("tf32", cg, 20000, stream.cuda_stream)
+            t, mhz, pms = _native.mma_peak("tf32", cg, 150000, stream.cuda_stream)
+            if best is None or t > best[0]:
+                best = (t, mhz, pms, cg)
+        sms = torch.cuda.get_device_properties(local).multi_processor_count
+        probe = {"tf32_tflops": best[0], "sm_mhz": best[1], "ms": best[2], "cta_group": best[3],
+                 "tf32_flop_per_clk_per_sm": best[0] * 1e12 / (best[1] * 1e6) / sms}
+    committed, committed_src = load_mma_peak()
+    if probe:
+        p_c = probe["tf32_tflops"] / 3.0
+        peak_src = (f"live tnx_mma_peak: tcgen05.mma kind::tf32 MMA-only loop, cta_group::{probe['cta_group']}, "
+                    f"{probe['tf32_tflops']:.1f} TFLOP/s at {probe['sm_mhz']:.0f} MHz (CTA clock64/globaltimer) "
+                    f"/ 3 split-TF32 passes")
+    elif committed:
+        p_c = committed["complex_3xtf32_peak_tflops"]
+        peak_src = f"{committed_src}: MMA-only kind::tf32 {committed['tf32_peak_tflops']:.1f} TFLOP/s / 3"
+    else:
+        p_c = peaks["bf16_tflops"] / 2.0 / 3.0
+        peak_src = (f"{peak_kind} MEASURED_PEAKS bf16_tflops {peaks['bf16_tflops']} / 2 (TF32 = half the "
+                    f"BF16 tensor rate) / 3 (split-TF32 passes)")
     achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
     traffic = load_traffic()
     # per-vertex roofline of the dominant contractions (top vertices covering
@@ -428,13 +488,18 @@ def main():
                                  str(traffic.get("algorithmic_bytes"))) if traffic else None,
                 "kernel": "gemm_c64_3xtf32 (tcgen05.mma.kind::tf32, 4M x 3 split passes)",
                 "peak_source": peak_src,
+                "mma_probe": probe,
+                # the same ceiling rescaled to the SM clock sampled during the timed slices
+                "peak_at_timed_clock": (probe["tf32_flop_per_clk_per_sm"] * torch.cuda.get_device_properties(
+                    local).multi_processor_count * clocks["sm_mhz"] * 1e6 / 1e12 / 3.0
+                    if probe and clocks.get("sm_mhz") else None),
+                "measured_peaks_bf16_context": peaks["bf16_tflops"] / 2.0 / 3.0,
                 "gemm_share_of_slice": gemm_ms / slice_ms if slice_ms else None,
                 "gemm_launches_per_slice": n_gemm,
                 "time_share_ms": {k: round(t, 3) for k, t in by_kind.items()},
                 "dominant_vertices": dom,
                 "dominant_min_frac": min((d["frac"] for d in dom), default=None),
-                # context: NVIDIA's nominal dense TF32 (1.1 PFLOP/s, B200_PROFILING.md) / 3 passes;
-                # MEASURED_PEAKS' cuBLAS bf16 ran at the clocks it saw, hence fractions above 1
+                # context: NVIDIA's nominal dense TF32 (1.1 PFLOP/s, B200_PROFILING.md) / 3 passes
                 "nominal_peak": NOMINAL_TF32 / 3.0,
                 "frac_nominal": achieved / (NOMINAL_TF32 / 3.0),
                 "dominant_min_frac_nominal": min((d["tflops"] / (NOMINAL_TF32 / 3.0) for d in dom), default=None),
@@ -505,6 +570,8 @@ def main():
                            "tree_source": meta["tree_source"], "precision": args.precision,
                            "ws_auto": meta.get("ws_auto")},
                 "slices_per_s": slices_per_s,
+                "zero_slice_fraction": timed_zero,
+                "sustained": sustained,
                 "roofline": roofline, "cpu_baseline": cpu, "parity": parity,
                 "e2e": e2e, "clocks": clocks,
                 "gpu_launches": K * st["launches_per_slice"],

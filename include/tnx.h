@@ -190,6 +190,16 @@ int tnx_synchronize(void* plan);
 int tnx_gemm_c64(const void* A, const void* B, void* C, int64_t batch, int64_t M,
                  int64_t N, int64_t K, int32_t precision, void* stream);
 
+/* Tensor-pipe ceiling (diagnostic; the denominator of the GEMM roofline):
+ * an MMA-only loop of `iters` tcgen05.mma (N=256; M=128 per CTA, or M=256
+ * per CTA pair with cta_group 2) over shared-memory-resident pseudo-random
+ * operands, one CTA per SM, no TMA / promotion / epilogue.  kind 0 =
+ * kind::tf32 (K=8), 1 = kind::f16 with BF16 operands (K=16).  Returns dense
+ * TFLOP/s over the device (2*M*N*K per MMA), the median SM clock the CTAs
+ * measured (clock64 / globaltimer) and the event-timed duration. */
+int tnx_mma_peak(int32_t kind, int32_t cta_group, int64_t iters, void* stream, double* tflops,
+                 double* sm_mhz, double* ms);
+
 #ifdef __cplusplus
 }
 #endif

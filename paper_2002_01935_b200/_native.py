@@ -78,6 +78,8 @@ SIGNATURES = {
                                     C.POINTER(C.c_int32)]),
     "tnx_gemm_c64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
                                C.c_int64, C.c_int32, C.c_void_p]),
+    "tnx_mma_peak": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_void_p, C.POINTER(C.c_double),
+                               C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }
 
 _lib = None
@@ -119,3 +121,12 @@ def check(rc):
         if rc == TNX_ERR_OOM:
             raise MemoryError(msg)
         raise NativeError(rc, msg)
+
+
+def mma_peak(kind="tf32", cta_group=2, iters=200000, stream=None):
+    """Tensor-pipe ceiling measured by ``tnx_mma_peak``: (TFLOP/s, SM MHz, ms)."""
+    lib = load()
+    t, m, ms = C.c_double(), C.c_double(), C.c_double()
+    check(lib.tnx_mma_peak({"tf32": 0, "bf16": 1}[kind], cta_group, iters, stream, C.byref(t), C.byref(m),
+                           C.byref(ms)))
+    return t.value, m.value, ms.value

@@ -33,6 +33,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <algorithm>
+#include <vector>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include "tnx_kernels.h"
@@ -168,6 +169,7 @@ struct GemmArgs {
   int32_t dstack;        // direct planes of a stacked-B parent operand: also write -im_hi, -im_lo (planes 4, 5)
   int32_t ksnake;        // odd waves traverse K in reverse (L2 reuse across waves)
   int32_t first;         // k-blocks of a unit's first TMEM round (>= promote; see launch_gemm)
+  float rz_kappa;        // round-toward-zero compensation (see the promotion loop); 0 disables
 };
 
 __device__ __forceinline__ int64_t map_offset(const IdxMap& m, int64_t idx) {
@@ -221,10 +223,10 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& g, float2* out, i
         float rh[4], rl[4], ih[4], il[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-          rh[t] = __uint_as_float(__float_as_uint(mre[j + t]) & 0xffffe000u);
-          ih[t] = __uint_as_float(__float_as_uint(mim[j + t]) & 0xffffe000u);
-          rl[t] = mre[j + t] - rh[t];
-          il[t] = mim[j + t] - ih[t];
+          rh[t] = tf32_hi(mre[j + t]);
+          ih[t] = tf32_hi(mim[j + t]);
+          rl[t] = tf32_lo(mre[j + t], rh[t]);
+          il[t] = tf32_lo(mim[j + t], ih[t]);
         }
         *reinterpret_cast<float4*>(d + off) = make_float4(rh[0], rh[1], rh[2], rh[3]);
         *reinterpret_cast<float4*>(d + off + ps) = make_float4(rl[0], rl[1], rl[2], rl[3]);
@@ -247,19 +249,20 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& g, float2* out, i
       if (col0 + j >= g.N) continue;
       const int64_t off = f + gtab[hcol + j];
       const float re = mre[j], im = mim[j];
-      const float rh = __uint_as_float(__float_as_uint(re) & 0xffffe000u);
-      const float ih = __uint_as_float(__float_as_uint(im) & 0xffffe000u);
+      const float rh = tf32_hi(re);
+      const float ih = tf32_hi(im);
       d[off] = rh;
       d[off + 2 * ps] = ih;
       if constexpr (MIX) {
         store_mix_x(d + ps, off, re, g.dside);
         store_mix_x(d + 3 * ps, off, im, g.dside);
       } else {
-        d[off + ps] = re - rh;
-        d[off + 3 * ps] = im - ih;
+        const float il = tf32_lo(im, ih);
+        d[off + ps] = tf32_lo(re, rh);
+        d[off + 3 * ps] = il;
         if (g.dstack) {
           d[off + 4 * ps] = -ih;
-          d[off + 5 * ps] = ih - im;
+          d[off + 5 * ps] = -il;
         }
       }
     }
@@ -642,11 +645,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mre[j] = 0.f;
         mim[j] = 0.f;
       }
+      const int F = min(nkb, max(P, g.first));
       for (int r = 0; r < rounds; ++r, ++R) {
         const uint32_t set = R & 1u;
         mbar_wait(smem_addr(&tfull[set]), (R >> 1) & 1u);
         tc_fence_after();
         const uint32_t t0 = lane_base + set * 256;
+        // Round-toward-zero compensation.  The tensor core truncates the FP32
+        // accumulator after every MMA, so each of the round's 12 MMAs per
+        // k-block (6 per 8-wide k-step: four split cross terms, then the two
+        // hi*hi terms) shrinks the partial sum S_j by 0.5 ulp(S_j) on average,
+        // i.e. by E[ulp/|S|]/2 = 2^-24 / (2 ln 2) ~ 0.72 * 2^-24 relative for
+        // log-uniformly distributed mantissas.  With exchangeable k-step
+        // increments E[S_j | S] is linear in j, so the expected shrink of the
+        // round's sum S is 2^-24 kappa (6 n_kb - 2) S (n_kb k-blocks per round;
+        // the four cross-term MMAs of a k-step act on the previous k-step's
+        // partial).  Promotion adds S (1 + that) -- an unbiased estimate, so the
+        // residual error is the zero-mean part that grows like sqrt(n).
+        const int nkb_r = r == 0 ? F : min(nkb - F - (r - 1) * P, P);
+        const float delta = g.rz_kappa * 5.9604645e-8f * (float)(6 * nkb_r - 2);
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           uint32_t re[32], im[32];
@@ -655,8 +672,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tmem_wait_ld();
 #pragma unroll
           for (int t = 0; t < 32; ++t) {
-            mre[j * 32 + t] += __uint_as_float(re[t]);
-            mim[j * 32 + t] += __uint_as_float(im[t]);
+            const float vr = __uint_as_float(re[t]), vi = __uint_as_float(im[t]);
+            mre[j * 32 + t] = fmaf(vr, delta, mre[j * 32 + t] + vr);
+            mim[j * 32 + t] = fmaf(vi, delta, mim[j * 32 + t] + vi);
           }
         }
         tc_fence_before();
@@ -972,6 +990,10 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
     // accumulation gets longer, so long-K accuracy is unchanged)
     static const int first = getenv("TNX_GEMM_FIRST") ? atoi(getenv("TNX_GEMM_FIRST")) : 6;
     a.first = g.promote > 0 ? 0 : first;
+    // kappa of the round-toward-zero compensation (TNX_GEMM_RZC; 0 disables);
+    // the mixed TF32/BF16 mode has another MMA sequence and is not compensated
+    static const float kappa = getenv("TNX_GEMM_RZC") ? (float)atof(getenv("TNX_GEMM_RZC")) : 0.0f;
+    a.rz_kappa = g.mix ? 0.0f : kappa;
   }
   const int splits = g.splits > 1 ? g.splits : 1;
   a.kb_per_split = (a.num_kb + splits - 1) / splits;
@@ -1035,6 +1057,178 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
   launch_pdl(splitk_reduce_kernel, blocks, 256, 0, st, reinterpret_cast<const float4*>(g.partial),
                                                reinterpret_cast<float4*>(g.out), n4, n4, zs);
   return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Tensor-pipe ceiling: an MMA-only loop (no TMA, no promotion, no epilogue)
+// over operands resident in shared memory, one CTA (or CTA pair) per SM.
+// Issues `iters` tcgen05.mma of N=256 (M=128 per CTA, M=256 per pair with
+// cta_group::2) alternating between two TMEM accumulator sets and two k-steps
+// of the same SWIZZLE_64B tiles the GEMM uses, so the per-MMA shared-memory
+// operand reads match the stacked-B GEMM's.  Operands are pseudo-random
+// (realistic switching power).  Each CTA records its clock64 and globaltimer
+// deltas, giving the SM clock the ceiling was measured at.
+namespace {
+constexpr int PEAK_THREADS = 128;
+constexpr int PEAK_A = BM * BK * 4;     // 8 KB: 128 rows x 64 B
+constexpr int PEAK_B = 2 * BN * BK * 4; // 16 KB: up to 256 rows x 64 B
+constexpr int PEAK_SMEM = 200 * 1024;   // one CTA per SM
+
+__device__ __forceinline__ uint32_t peak_hash(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352dU;
+  x ^= x >> 15;
+  x *= 0x846ca68bU;
+  x ^= x >> 16;
+  return x;
+}
+
+template <bool TWO_SM, bool BF16>
+__global__ void __launch_bounds__(PEAK_THREADS, 1)
+    mma_peak_kernel(int64_t iters, unsigned long long* rec) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* done = reinterpret_cast<uint64_t*>(smem + PEAK_A + PEAK_B);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const uint32_t rank = TWO_SM ? cluster_rank() : 0u;
+  // pseudo-random operands in [-1, 1): fp32 bits, or bf16 pairs
+  for (int i = threadIdx.x; i < (PEAK_A + PEAK_B) / 4; i += PEAK_THREADS) {
+    const uint32_t h = peak_hash((uint32_t)i * 2654435761u + blockIdx.x * 97u + 1u);
+    uint32_t v;
+    if (BF16) {
+      const float lo = (float)(int)(h & 0xffffu) / 32768.0f - 1.0f;
+      const float hi = (float)(int)(h >> 16) / 32768.0f - 1.0f;
+      v = (__float_as_uint(lo) >> 16) | (__float_as_uint(hi) & 0xffff0000u);
+    } else {
+      v = __float_as_uint((float)(int)(h >> 8) / 8388608.0f - 1.0f);
+    }
+    reinterpret_cast<uint32_t*>(smem)[i] = v;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x < 32) {
+    if constexpr (TWO_SM) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_addr(tmem_slot)), "r"(TMEM_COLS) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_addr(tmem_slot)), "r"(TMEM_COLS) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+  }
+  if (threadIdx.x == 32) {
+    mbar_init(smem_addr(done), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  if constexpr (TWO_SM) cluster_sync_all(); else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  unsigned long long c0 = clock64(), g0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+  if (threadIdx.x == 32 && rank == 0) {
+    constexpr uint32_t ID = idesc_mma<TWO_SM>(false, BF16 ? 1u : 2u, 2 * BN);
+    const uint32_t sa = smem_addr(smem), sb = smem_addr(smem + PEAK_A);
+    for (int64_t i = 0; i < iters; ++i) {
+      const uint32_t koff = (uint32_t)(i & 1) * 32u;
+      const uint32_t d = tmem_base + (uint32_t)((i >> 1) & 1) * 256u;
+      const uint32_t acc = i >= 4 ? 1u : 0u;
+      const uint64_t a = umma_desc_sw64(sa + koff), b = umma_desc_sw64(sb + koff);
+      if constexpr (TWO_SM) {
+        if (BF16) umma_bf16_2sm(d, a, b, ID, acc); else umma_tf32_2sm(d, a, b, ID, acc);
+      } else {
+        if (BF16) umma_bf16(d, a, b, ID, acc); else umma_tf32(d, a, b, ID, acc);
+      }
+    }
+    if constexpr (TWO_SM) umma_commit_2sm(smem_addr(done)); else umma_commit(smem_addr(done));
+  }
+  if (threadIdx.x == 0) mbar_wait(smem_addr(done), 0);
+  __syncthreads();
+  tc_fence_after();
+  const unsigned long long c1 = clock64();
+  unsigned long long g1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+  if (threadIdx.x == 0) {
+    rec[2 * blockIdx.x] = c1 - c0;
+    rec[2 * blockIdx.x + 1] = g1 - g0;
+  }
+  tc_fence_before();
+  if constexpr (TWO_SM) cluster_sync_all(); else __syncthreads();
+  if (threadIdx.x < 32) {
+    tc_fence_after();
+    if constexpr (TWO_SM)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                   : "memory");
+  }
+}
+
+template <bool TWO_SM, bool BF16>
+cudaError_t launch_mma_peak(int64_t iters, unsigned long long* rec, int grid, cudaStream_t st) {
+  auto k = mma_peak_kernel<TWO_SM, BF16>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, PEAK_SMEM);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(PEAK_THREADS);
+  cfg.dynamicSmemBytes = PEAK_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = TWO_SM ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = TWO_SM ? 1 : 0;
+  e = cudaLaunchKernelEx(&cfg, k, iters, rec);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+}  // namespace
+
+int gemm_mma_peak(int bf16, int two_sm, int64_t iters, cudaStream_t st, double* tflops, double* sm_mhz,
+                  double* ms, char* err, size_t errlen) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = two_sm ? (sms / 2) * 2 : sms;
+  unsigned long long* rec = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaError_t e = cudaMalloc(&rec, sizeof(unsigned long long) * 2 * grid);
+  if (e == cudaSuccess) e = cudaEventCreate(&e0);
+  if (e == cudaSuccess) e = cudaEventCreate(&e1);
+  auto launch = [&](int64_t n) {
+    if (two_sm) return bf16 ? launch_mma_peak<true, true>(n, rec, grid, st) : launch_mma_peak<true, false>(n, rec, grid, st);
+    return bf16 ? launch_mma_peak<false, true>(n, rec, grid, st) : launch_mma_peak<false, false>(n, rec, grid, st);
+  };
+  float t = 0.f;
+  if (e == cudaSuccess) e = launch(std::min<int64_t>(iters, 4096));  // warm-up
+  if (e == cudaSuccess) e = cudaEventRecord(e0, st);
+  if (e == cudaSuccess) e = launch(iters);
+  if (e == cudaSuccess) e = cudaEventRecord(e1, st);
+  if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+  if (e == cudaSuccess) e = cudaEventElapsedTime(&t, e0, e1);
+  std::vector<unsigned long long> h(2 * grid);
+  if (e == cudaSuccess) e = cudaMemcpy(h.data(), rec, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  if (rec) cudaFree(rec);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (e != cudaSuccess) {
+    snprintf(err, errlen, "mma peak: %s", cudaGetErrorString(e));
+    return 1;
+  }
+  // flop per MMA per CTA: 2 * 128 rows * 256 columns * K (8 tf32 / 16 bf16)
+  const double flop = (double)grid * (double)iters * 2.0 * BM * 2 * BN * (bf16 ? 16 : 8);
+  *ms = t;
+  *tflops = flop / (t * 1e-3) / 1e12;
+  std::vector<double> mhz;
+  for (int i = 0; i < grid; ++i)
+    if (h[2 * i + 1] > 0) mhz.push_back(1e3 * (double)h[2 * i] / (double)h[2 * i + 1]);
+  std::sort(mhz.begin(), mhz.end());
+  *sm_mhz = mhz.empty() ? 0.0 : mhz[mhz.size() / 2];
+  return 0;
 }
 
 }  // namespace tnx

@@ -334,19 +334,20 @@ __global__ void __launch_bounds__(256) pack_kernel(const PackParams p) {
       re = v.x;
       im = v.y;
     }
-    const float re_hi = __uint_as_float(__float_as_uint(re) & 0xffffe000u);
-    const float im_hi = __uint_as_float(__float_as_uint(im) & 0xffffe000u);
+    const float re_hi = tf32_hi(re);
+    const float im_hi = tf32_hi(im);
     p.dst[e] = re_hi;
     p.dst[e + 2 * p.plane_stride] = im_hi;
     if (p.mix) {
       store_mix_x(p.dst + p.plane_stride, e, re, p.mix == 2);
       store_mix_x(p.dst + 3 * p.plane_stride, e, im, p.mix == 2);
     } else {
-      p.dst[e + p.plane_stride] = re - re_hi;
-      p.dst[e + 3 * p.plane_stride] = im - im_hi;
+      const float im_lo = tf32_lo(im, im_hi);
+      p.dst[e + p.plane_stride] = tf32_lo(re, re_hi);
+      p.dst[e + 3 * p.plane_stride] = im_lo;
       if (p.nplanes == 6) {  // stacked-B operand: negated imaginary planes
         p.dst[e + 4 * p.plane_stride] = -im_hi;
-        p.dst[e + 5 * p.plane_stride] = im_hi - im;
+        p.dst[e + 5 * p.plane_stride] = -im_lo;
       }
     }
   }
@@ -425,15 +426,16 @@ __global__ void __launch_bounds__(256) perm_kernel(const PermParams p) {
         static_cast<float2*>(p.dst)[off] = v;
       } else {
         float* d = static_cast<float*>(p.dst);
-        const float re_hi = __uint_as_float(__float_as_uint(v.x) & 0xffffe000u);
-        const float im_hi = __uint_as_float(__float_as_uint(v.y) & 0xffffe000u);
+        const float re_hi = tf32_hi(v.x);
+        const float im_hi = tf32_hi(v.y);
+        const float im_lo = tf32_lo(v.y, im_hi);
         d[off] = re_hi;
-        d[off + p.plane_stride] = v.x - re_hi;
+        d[off + p.plane_stride] = tf32_lo(v.x, re_hi);
         d[off + 2 * p.plane_stride] = im_hi;
-        d[off + 3 * p.plane_stride] = v.y - im_hi;
+        d[off + 3 * p.plane_stride] = im_lo;
         if (p.mode == 2) {
           d[off + 4 * p.plane_stride] = -im_hi;
-          d[off + 5 * p.plane_stride] = im_hi - v.y;
+          d[off + 5 * p.plane_stride] = -im_lo;
         }
       }
     }
@@ -560,10 +562,10 @@ __global__ void __launch_bounds__(256, DOT ? 3 : 4) perm_vec_kernel(const PermPa
       if (p.mode == 0) {
         __stcs(reinterpret_cast<float4*>(static_cast<float2*>(p.dst) + off), v);
       } else {
-        const float ar = __uint_as_float(__float_as_uint(v.x) & 0xffffe000u);
-        const float ai = __uint_as_float(__float_as_uint(v.y) & 0xffffe000u);
-        const float br = __uint_as_float(__float_as_uint(v.z) & 0xffffe000u);
-        const float bi = __uint_as_float(__float_as_uint(v.w) & 0xffffe000u);
+        const float ar = tf32_hi(v.x);
+        const float ai = tf32_hi(v.y);
+        const float br = tf32_hi(v.z);
+        const float bi = tf32_hi(v.w);
         *reinterpret_cast<float2*>(d + off) = make_float2(ar, br);
         *reinterpret_cast<float2*>(d + off + 2 * p.plane_stride) = make_float2(ai, bi);
         if (p.mode >= 3) {
@@ -572,11 +574,12 @@ __global__ void __launch_bounds__(256, DOT ? 3 : 4) perm_vec_kernel(const PermPa
           store_mix_x(d + 3 * p.plane_stride, off, v.y, p.mode == 4);
           store_mix_x(d + 3 * p.plane_stride, off + 1, v.w, p.mode == 4);
         } else {
-          *reinterpret_cast<float2*>(d + off + p.plane_stride) = make_float2(v.x - ar, v.z - br);
-          *reinterpret_cast<float2*>(d + off + 3 * p.plane_stride) = make_float2(v.y - ai, v.w - bi);
+          const float ail = tf32_lo(v.y, ai), bil = tf32_lo(v.w, bi);
+          *reinterpret_cast<float2*>(d + off + p.plane_stride) = make_float2(tf32_lo(v.x, ar), tf32_lo(v.z, br));
+          *reinterpret_cast<float2*>(d + off + 3 * p.plane_stride) = make_float2(ail, bil);
           if (p.mode == 2) {  // stacked-B operand: negated imaginary planes
             *reinterpret_cast<float2*>(d + off + 4 * p.plane_stride) = make_float2(-ai, -bi);
-            *reinterpret_cast<float2*>(d + off + 5 * p.plane_stride) = make_float2(ai - v.y, bi - v.w);
+            *reinterpret_cast<float2*>(d + off + 5 * p.plane_stride) = make_float2(-ail, -bil);
           }
         }
       }

@@ -169,9 +169,21 @@ struct AccumParams {
 // 16-wide k-block row, 32 bf16 = [hi(16) | lo(16)] for the A operand and
 // [lo(16) | hi(16)] for B, so one bf16 MMA chunk pairs A.hi with B.lo and the
 // next A.lo with B.hi (the two cross terms of the split product).
-__device__ __forceinline__ float tf32_hi(float v) {
-  return __uint_as_float(__float_as_uint(v) & 0xffffe000u);
+// Split-TF32 operands: hi = v rounded to nearest TF32, lo = (v - hi) rounded to
+// nearest TF32.  Round-to-nearest on both parts keeps the split unbiased: the
+// dropped lo*lo term and the residual v - hi - lo (<= 2^-22 |v|) carry random
+// signs.  (Truncation -- masking the low 13 bits -- would make lo share the
+// sign of v, so every dropped term would shrink |product| by ~1e-7 and the
+// shrink would compound multiplicatively along the tree's GEMM chain.  The
+// tensor core reads only the TF32 bits of each operand, so lo must itself be a
+// TF32 value.)
+__device__ __forceinline__ float tf32_rn(float v) {
+  uint32_t r;
+  asm("cvt.rn.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+  return __uint_as_float(r);
 }
+__device__ __forceinline__ float tf32_hi(float v) { return tf32_rn(v); }
+__device__ __forceinline__ float tf32_lo(float v, float hi) { return tf32_rn(v - hi); }
 __device__ __forceinline__ void store_mix_x(float* plane_x, int64_t e, float v, int side_b) {
   const float hi = tf32_hi(v);
   const float lo = v - hi;
@@ -248,5 +260,8 @@ int gemm_stack_enabled();
 int gemm_use_stack(int64_t batch, int64_t M, int64_t N, int64_t kp, int two_sm);
 cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st);
 int gemm_init_attributes(char* err, size_t errlen);
+// MMA-only tensor-pipe ceiling (no TMA / epilogue): TFLOP/s, median SM MHz
+int gemm_mma_peak(int bf16, int two_sm, int64_t iters, cudaStream_t st, double* tflops, double* sm_mhz,
+                  double* ms, char* err, size_t errlen);
 
 }  // namespace tnx
