@@ -395,13 +395,16 @@ def main():
             if use_dist:
                 dist.all_reduce(ms2, op=dist.ReduceOp.MAX)
             ms2 = float(ms2.item())
-            sample = list(range(s_base, s_base + n_s, max(1, n_s // 48)))
+            # a contiguous block (zero slices follow the sliced labels' digit
+            # pattern, so a strided sample can alias with it)
+            mid = s_base + max(0, n_s // 2 - 24)
+            sample = list(range(mid, min(s_base + n_s, mid + 48)))
             sustained = {"value": n_s * world * flops_slice / (ms2 / 1e3) / 1e12, "unit": "TFLOP/s",
                          "seconds": ms2 / 1e3, "slices_per_rank": n_s, "ms_per_step": ms2 / n_s,
                          "slices_per_s": n_s * world / (ms2 / 1e3), "clocks": clocks2,
                          "zero_slice_fraction": zero_fraction(slice_values(sample))
                          if st["out_elements"] == 1 else None,
-                         "zero_sample": f"{len(sample)} slices spread over the sustained range"}
+                         "zero_sample": f"{len(sample)} consecutive slices from the middle of the sustained range"}
 
     # per-launch profile of one slice (CUDA events on the launching stream)
     prof_b = plan.profile_slice(base + W, with_bytes=True)
@@ -418,18 +421,27 @@ def main():
     # by 3 (split-TF32: 24 M N K real tensor flop per 8 M N K complex flop).
     from paper_2002_01935_b200 import _native
     probe = None
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
     if not args.no_tf32_probe:
         best = None
         for cg in (2, 1):
             _native.mma_peak("tf32", cg, 20000, stream.cuda_stream)
             t, mhz, pms = _native.mma_peak("tf32", cg, 150000, stream.cuda_stream)
-            if best is None or t > best[0]:
+            if best is None or t / mhz > best[0] / best[1]:
                 best = (t, mhz, pms, cg)
-        sms = torch.cuda.get_device_properties(local).multi_processor_count
         probe = {"tf32_tflops": best[0], "sm_mhz": best[1], "ms": best[2], "cta_group": best[3],
                  "tf32_flop_per_clk_per_sm": best[0] * 1e12 / (best[1] * 1e6) / sms}
     committed, committed_src = load_mma_peak()
-    if probe:
+    if probe and clocks.get("sm_mhz"):
+        # the probe's per-clock rate at the clock the timed slices ran at (the
+        # MMA-only loop on random operands draws more power than the GEMM and
+        # runs at a lower clock, so its raw TFLOP/s would understate the ceiling)
+        p_c = probe["tf32_flop_per_clk_per_sm"] * sms * clocks["sm_mhz"] * 1e6 / 1e12 / 3.0
+        peak_src = (f"live tnx_mma_peak (tcgen05.mma kind::tf32 MMA-only loop, cta_group::{probe['cta_group']}): "
+                    f"{probe['tf32_flop_per_clk_per_sm']:.0f} flop/clk/SM x {sms} SMs x {clocks['sm_mhz']:.0f} MHz "
+                    f"(median SM clock sampled during the timed slices) / 3 split-TF32 passes; raw probe "
+                    f"{probe['tf32_tflops']:.1f} TFLOP/s at {probe['sm_mhz']:.0f} MHz")
+    elif probe:
         p_c = probe["tf32_tflops"] / 3.0
         peak_src = (f"live tnx_mma_peak: tcgen05.mma kind::tf32 MMA-only loop, cta_group::{probe['cta_group']}, "
                     f"{probe['tf32_tflops']:.1f} TFLOP/s at {probe['sm_mhz']:.0f} MHz (CTA clock64/globaltimer) "
@@ -489,10 +501,7 @@ def main():
                 "kernel": "gemm_c64_3xtf32 (tcgen05.mma.kind::tf32, 4M x 3 split passes)",
                 "peak_source": peak_src,
                 "mma_probe": probe,
-                # the same ceiling rescaled to the SM clock sampled during the timed slices
-                "peak_at_timed_clock": (probe["tf32_flop_per_clk_per_sm"] * torch.cuda.get_device_properties(
-                    local).multi_processor_count * clocks["sm_mhz"] * 1e6 / 1e12 / 3.0
-                    if probe and clocks.get("sm_mhz") else None),
+                "probe_peak_raw": probe["tf32_tflops"] / 3.0 if probe else None,
                 "measured_peaks_bf16_context": peaks["bf16_tflops"] / 2.0 / 3.0,
                 "gemm_share_of_slice": gemm_ms / slice_ms if slice_ms else None,
                 "gemm_launches_per_slice": n_gemm,

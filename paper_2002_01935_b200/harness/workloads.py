@@ -29,6 +29,8 @@ CONFIGS = {
                            desc="20x20 OBC square lattice, bond dim 2, scalar"),
     "cfg4_7x7_d40": dict(make=lambda: gen.grid_circuit(7, 7, 40, seed=0), ws=27,
                          desc="rectangular 7x7 (1+40+1) random circuit amplitude, 742 rank-3 tensors"),
+    "cfg4g_7x7_d40": dict(make=lambda: gen.grid_circuit(7, 7, 40, seed=0), ws=27,
+                          desc="7x7 (1+40+1) circuit amplitude, greedy-driver tree (round-1 bench tree)"),
     # parity-only companions of cfg4 (same generator, shallower): the full
     # amplitude is computable by the CPU oracle
     "cfg4p_7x7_d16": dict(make=lambda: gen.grid_circuit(7, 7, 16, seed=0), ws=16,

@@ -9,8 +9,10 @@ seeded networks, trees and slice sets and compare against the stored values.
 
 * ``d24``  -- every slice of the 7x7 (1+24+1) amplitude at W_s=27 (32 slices,
   reference min-fill tree): per-slice values and the full amplitude.
-* ``d40``  -- slices 0..15 of the bench workload (7x7 (1+40+1), W_s=27).
+* ``d40``  -- slices 0..15 of the bench workload (7x7 (1+40+1), W_s=27,
+  reference min-fill tree).
 * ``d40r`` -- 8 seeded random slice ids of the same workload.
+* ``d40g`` / ``d40gr`` -- the same for the greedy-driver tree (cfg4g).
 
 Per slice it stores the value, its root-operand scale ||x|| ||y|| (the
 condition of the last contraction) and the slice's label assignment digits, so
@@ -38,6 +40,9 @@ SETS = {
     "d24": ("cfg4p_7x7_d24", 27, "all"),
     "d40": ("cfg4_7x7_d40", 27, list(range(16))),
     "d40r": ("cfg4_7x7_d40", 27, "random8"),
+    # the same circuit under the greedy-driver tree (round-1 bench workload)
+    "d40g": ("cfg4g_7x7_d40", 27, list(range(16))),
+    "d40gr": ("cfg4g_7x7_d40", 27, "random8"),
 }
 
 

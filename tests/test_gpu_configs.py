@@ -1,8 +1,15 @@
 """Parity of the five BASELINE.json configurations (reference-driver trees,
 greedy_slice slice sets) at slice widths the CPU oracle finishes in seconds.
-Tolerance: |c_gpu - c_ref| <= 1e-5 |c_ref| + 1e-6 ||x_root|| ||y_root||
-(the second term only matters for slices that are zero or nearly zero in
-exact arithmetic, common in sliced circuits)."""
+
+Tolerance (cond = ||x_root|| ||y_root|| / |c_ref|, the cancellation of the
+root contraction):
+* circuit amplitudes (cfg4, cfg5): plain relative |c_gpu - c_ref| <= 1e-5 |c_ref|;
+  a slice that is zero in exact arithmetic (cond > 1e12: the oracle's own
+  value is complex128 round-off) must stay below 1e-9 ||x|| ||y||;
+* random networks (cfg1-3: iid complex leaves, values with heavy cancellation):
+  |c_gpu - c_ref| <= 1e-5 |c_ref| + 1e-9 ||x|| ||y||, i.e. plain 1e-5 until
+  cond ~ 1e4 -- complex64 storage alone gives ~6e-8 ||x|| ||y|| / sqrt(n) of
+  irreducible error."""
 import numpy as np
 import pytest
 
@@ -19,7 +26,7 @@ CASES = [("cfg1_3reg50", None, 3), ("cfg2_5reg100", 24, 3), ("cfg3_lattice20", N
 #  oracle's hyperedge contractions at depth 40 / W_s=24 take ~10 minutes)
 
 
-def _root_check(tn, tree, ss, plan, s):
+def _root_check(name, tn, tree, ss, plan, s):
     rec = {}
     keep = {tree.root, *tree.children(tree.root)}
 
@@ -35,7 +42,16 @@ def _root_check(tn, tree, ss, plan, s):
     plan.run(s, s + 1)
     got = plan.result()
     err = np.linalg.norm(np.ravel(got - ref))
-    assert err <= 1e-5 * np.linalg.norm(np.ravel(ref)) + 1e-6 * scale, (s, got, ref, scale)
+    nref = np.linalg.norm(np.ravel(ref))
+    cond = scale / nref if nref > 0 else float("inf")
+    circuit = name.startswith(("cfg4", "cfg5"))
+    print(f"{name} slice {s}: rel {err / nref if nref else float('nan'):.2e} cond {cond:.1e}")
+    if circuit and cond > 1e12:
+        assert err <= 1e-9 * scale, (s, got, ref, scale)
+    elif circuit:
+        assert err <= 1e-5 * nref, (s, got, ref, err / nref, cond)
+    else:
+        assert err <= 1e-5 * nref + 1e-9 * scale, (s, got, ref, err / nref, cond)
     assert ops == plan.ops_per_slice
     return ref
 
@@ -49,7 +65,7 @@ def test_config_slices(name, ws, nslices):
         assert st["num_gemm"] > 0 or name == "cfg1_3reg50"
         ids = sorted({0, plan.d - 1, int(np.random.default_rng(0).integers(plan.d))})
         for s in ids[:nslices]:
-            _root_check(tn, tree, ss, plan, s)
+            _root_check(name, tn, tree, ss, plan, s)
         if plan.d == 1:
             # unsliced: the root check above already compared the full value;
             # also run it through the public entry point (graph + accumulate)

@@ -1,7 +1,12 @@
 """GPU parity: the B200 executor (through the C ABI) vs the CPU oracle and the
 reference golden vectors.  Tolerance: complex64 execution vs complex128
-reference, norm-wise relative error <= 1e-5 (north_star), with an absolute
-floor of 1e-5 * (value of the |.|-network) for cancelling random cases."""
+reference, norm-wise relative error <= 1e-5 (north_star).  Random networks
+(iid complex leaves) cancel heavily, so for them (check_close with the
+network) the bound is 1e-5 * max(|ref|, 1e-2 * |.|-network value): an
+absolute floor of 1e-7 times the value of the network with every entry
+replaced by its modulus -- the scale of the forward error bound of a
+complex64 sum-of-products (about 2u = 1.2e-7 of it per rounding).  Circuit
+amplitudes use the plain relative error."""
 import numpy as np
 import pytest
 
