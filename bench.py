@@ -196,8 +196,13 @@ def run_reference(args):
     warm = min(args.warmup, 1)
     budget = args.ref_budget
     spent = 0.0
-    for i in range(warm + steps):
-        val, ops, dt, cores, _ = cpu_baseline(tn, tree, ss, i, budget)
+    nz_path = os.path.join(REPO, "benchdata", f"{args.config}.slices.json")
+    ids = list(range(warm + steps))
+    if args.slices == "nonzero" and os.path.exists(nz_path):
+        with open(nz_path) as fh:
+            ids = [int(x) for x in json.load(fh)["ids"]][:warm + steps]  # the b200 arm's rank-0 ids
+    for i in range(len(ids)):
+        val, ops, dt, cores, _ = cpu_baseline(tn, tree, ss, ids[i], budget)
         assert ops == per_slice
         spent += dt
         if i >= warm:
@@ -214,7 +219,8 @@ def run_reference(args):
                        "flops_per_slice": flops},
             "slices_per_s": len(times) / t,
             "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "port",
-                             "sample": f"{len(times)} full slice(s) of {args.config} (W_s={ss.Ws:g}), "
+                             "sample": f"{len(times)} full slice(s) of {args.config} (W_s={ss.Ws:g}; ids "
+                                       f"{ids[warm:warm + len(times)]}), "
                                        "oracle restatement of SPEC contract_sliced over the reference's "
                                        "pairwise_contract/fix_index semantics, complex128 numpy einsum"},
             "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -253,6 +259,9 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=90.0)
     ap.add_argument("--profile-out", default=None)
     ap.add_argument("--no-tf32-probe", action="store_true", help="skip the live MMA-only ceiling probe")
+    ap.add_argument("--slices", default="nonzero", choices=["nonzero", "prefix"],
+                    help="timed slice ids: the workload's nonzero-slice list (benchdata/<config>.slices.json) "
+                         "or the enumeration prefix")
     ap.add_argument("--sustained-s", type=float, default=10.0,
                     help="after the headline, time ~this many seconds of further slices (0: skip)")
     ap.add_argument("--no-direct", action="store_true", help="disable GEMM->GEMM operand-plane fusion")
@@ -303,15 +312,45 @@ def main():
     st = plan.stats()
     flops_slice = plan.flops_per_slice
     W, K = args.warmup, args.steps
-    if (W + K) * world * 2 > plan.d:
+    nz_path = os.path.join(REPO, "benchdata", f"{args.config}.slices.json")
+    use_list = args.slices == "nonzero" and os.path.exists(nz_path)
+    if use_list:
+        with open(nz_path) as fh:
+            nz_rec = json.load(fh)
+        nz_ids = [int(x) for x in nz_rec["ids"]]
+    elif (W + K) * world * 2 > plan.d:
         raise SystemExit("slice prefix larger than d_sliced")
     # an explicit stream: the legacy default stream has handle 0, which the C
     # ABI reads as "the library's own stream"
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    # the job contracts the prefix [0, world*(W+K)) of the slice enumeration;
-    # each rank owns one contiguous block (bit-exact sub-range)
+    # Which slices the job contracts.  "nonzero" (default when the workload has
+    # a benchdata/<config>.slices.json list): ids that are nonzero in exact
+    # arithmetic, found by tools/slice_scan.py -- the timed operands are then
+    # real amplitude data, not round-off of structurally zero slices (which
+    # draw less power); rank r takes the r-th block of W+K ids, cycling
+    # through the list.  "prefix": the prefix [0, world*(W+K)) of the slice
+    # enumeration, one contiguous block per rank (bit-exact sub-range).
     base, _ = slice_range(0, world * (W + K), world, rank)
+
+    def job_ids(offset, n):
+        if use_list:
+            return [nz_ids[(offset + i) % len(nz_ids)] for i in range(n)]
+        return list(range(offset, offset + n))
+
+    warm_ids = job_ids(rank * (W + K) if use_list else base, W)
+    timed_ids = job_ids(rank * (W + K) + W if use_list else base + W, K)
+
+    def run_ids(ids):
+        """Contract `ids` into the accumulator: contiguous runs go through one
+        tnx_run_slices call (graph replays), others one call per id."""
+        i = 0
+        while i < len(ids):
+            j = i + 1
+            while j < len(ids) and ids[j] == ids[j - 1] + 1:
+                j += 1
+            plan.run(ids[i], ids[j - 1] + 1, stream)
+            i = j
     red_dev = "cuda" if backend == "nccl" else "cpu"
 
     def barrier():
@@ -322,7 +361,7 @@ def main():
                 dist.barrier()
 
     # warm-up
-    plan.run(base, base + W, stream)
+    run_ids(warm_ids)
     torch.cuda.synchronize()
     plan.reset(stream)
     torch.cuda.synchronize()
@@ -334,7 +373,7 @@ def main():
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    plan.run(base + W, base + W + K, stream)
+    run_ids(timed_ids)
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -370,7 +409,7 @@ def main():
     total_slices = K * world
     value = total_slices * flops_slice / (ms_max / 1e3) / 1e12
     slices_per_s = total_slices / (ms_max / 1e3)
-    timed_zero = zero_fraction(slice_values(range(base + W, base + W + K))) if st["out_elements"] == 1 else None
+    timed_zero = zero_fraction(slice_values(timed_ids)) if st["out_elements"] == 1 else None
 
     # sustained: the same per-slice work for >= --sustained-s seconds (the GEMMs
     # run into the 1 kW power cap; the headline above is a ~0.5 s burst)
@@ -378,7 +417,8 @@ def main():
     if args.sustained_s > 0:
         n_s = max(K, int(math.ceil(args.sustained_s * 1e3 / (ms_max / K))))
         s_base = world * (W + K) + rank * n_s
-        if s_base + n_s <= plan.d:
+        sus_ids = job_ids(s_base, n_s)
+        if use_list or s_base + n_s <= plan.d:
             plan.reset(stream)
             clk2 = ClockSampler(local).start()
             barrier()
@@ -386,7 +426,7 @@ def main():
             f0 = torch.cuda.Event(enable_timing=True)
             f1 = torch.cuda.Event(enable_timing=True)
             f0.record(stream)
-            plan.run(s_base, s_base + n_s, stream)
+            run_ids(sus_ids)
             f1.record(stream)
             torch.cuda.synchronize()
             barrier()
@@ -397,8 +437,8 @@ def main():
             ms2 = float(ms2.item())
             # a contiguous block (zero slices follow the sliced labels' digit
             # pattern, so a strided sample can alias with it)
-            mid = s_base + max(0, n_s // 2 - 24)
-            sample = list(range(mid, min(s_base + n_s, mid + 48)))
+            mid = max(0, n_s // 2 - 24)
+            sample = sus_ids[mid:mid + 48]
             sustained = {"value": n_s * world * flops_slice / (ms2 / 1e3) / 1e12, "unit": "TFLOP/s",
                          "seconds": ms2 / 1e3, "slices_per_rank": n_s, "ms_per_step": ms2 / n_s,
                          "slices_per_s": n_s * world / (ms2 / 1e3), "clocks": clocks2,
@@ -407,7 +447,7 @@ def main():
                          "zero_sample": f"{len(sample)} consecutive slices from the middle of the sustained range"}
 
     # per-launch profile of one slice (CUDA events on the launching stream)
-    prof_b = plan.profile_slice(base + W, with_bytes=True)
+    prof_b = plan.profile_slice(timed_ids[0], with_bytes=True)
     prof = [(k, v, t) for k, v, t, b in prof_b]
     info = {v["ssa"]: v for v in plan.vertex_info()}
     gemm_ms = sum(t for k, v, t in prof if k == "gemm")
@@ -529,10 +569,9 @@ def main():
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        s0 = base + W
-        for i in range(K):
+        for sid_ in timed_ids:
             plan.bind(leaf_arrays=leaves, stream=stream)
-            plan.run(s0 + i, s0 + i + 1, stream)
+            plan.run(sid_, sid_ + 1, stream)
             plan.result(stream)
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
@@ -548,7 +587,7 @@ def main():
     cpu = None
     parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sid = base  # slice 0: non-degenerate (many slices of this circuit are exactly zero)
+        sid = timed_ids[0]
         plan.reset(stream)
         plan.run(sid, sid + 1, stream)
         gpu_val = complex(plan.result(stream))
@@ -576,6 +615,10 @@ def main():
                            "d_sliced": str(ss.d), "sliced_labels": len(ss.labels),
                            "flops_per_slice": flops_slice, "slices_per_rank": K,
                            "l2": "per-slice working set > L2 (no flush needed)",
+                           "slices": (f"nonzero slice ids ({len(nz_ids)} in benchdata/{args.config}.slices.json, "
+                                      f"nonzero fraction of a random sample {nz_rec['nonzero_fraction']:.3f}); "
+                                      f"rank r times ids [r*(W+K)+W, (r+1)*(W+K)) of the list, cyclic"
+                                      if use_list else f"prefix [0, {world * (W + K)}) of the enumeration"),
                            "tree_source": meta["tree_source"], "precision": args.precision,
                            "ws_auto": meta.get("ws_auto")},
                 "slices_per_s": slices_per_s,

@@ -9,9 +9,11 @@ seeded networks, trees and slice sets and compare against the stored values.
 
 * ``d24``  -- every slice of the 7x7 (1+24+1) amplitude at W_s=27 (32 slices,
   reference min-fill tree): per-slice values and the full amplitude.
-* ``d40``  -- slices 0..15 of the bench workload (7x7 (1+40+1), W_s=27,
-  reference min-fill tree).
-* ``d40r`` -- 8 seeded random slice ids of the same workload.
+* ``d40``  -- the first 16 ids of the bench workload's nonzero-slice list
+  (7x7 (1+40+1), W_s=27, reference min-fill tree; benchdata/
+  cfg4_7x7_d40.slices.json -- this tree's slices [0, 1024) are all zero in
+  exact arithmetic).
+* ``d40r`` -- 8 seeded picks from the rest of that list.
 * ``d40g`` / ``d40gr`` -- the same for the greedy-driver tree (cfg4g).
 
 Per slice it stores the value, its root-operand scale ||x|| ||y|| (the
@@ -38,17 +40,31 @@ OUT = os.path.join(HERE, "northstar_fixtures.json")
 
 SETS = {
     "d24": ("cfg4p_7x7_d24", 27, "all"),
-    "d40": ("cfg4_7x7_d40", 27, list(range(16))),
-    "d40r": ("cfg4_7x7_d40", 27, "random8"),
+    "d40": ("cfg4_7x7_d40", 27, "nonzero:0:16"),
+    "d40r": ("cfg4_7x7_d40", 27, "nonzero-random8"),
     # the same circuit under the greedy-driver tree (round-1 bench workload)
     "d40g": ("cfg4g_7x7_d40", 27, list(range(16))),
     "d40gr": ("cfg4g_7x7_d40", 27, "random8"),
 }
 
 
-def slice_ids(spec, d):
+def nonzero_ids(name):
+    """Slice ids of the workload that are nonzero in exact arithmetic
+    (benchdata/<name>.slices.json, found by tools/slice_scan.py)."""
+    with open(os.path.join(REPO, "benchdata", f"{name}.slices.json")) as fh:
+        return [int(x) for x in json.load(fh)["ids"]]
+
+
+def slice_ids(spec, d, name=None):
     if spec == "all":
         return list(range(d))
+    if isinstance(spec, str) and spec.startswith("nonzero:"):
+        a, b = (int(x) for x in spec.split(":")[1:])
+        return nonzero_ids(name)[a:b]
+    if spec == "nonzero-random8":
+        rest = nonzero_ids(name)[16:]
+        rng = np.random.default_rng(2002)
+        return sorted(int(rest[i]) for i in rng.choice(len(rest), size=8, replace=False))
     if spec == "random8":
         rng = np.random.default_rng(2002)
         return sorted(int(x) for x in rng.integers(0, d, size=8, dtype=np.int64))
@@ -58,7 +74,7 @@ def slice_ids(spec, d):
 def run(key):
     name, ws, spec = SETS[key]
     tn, tree, ss, meta = load_workload(name, ws=ws)
-    ids = slice_ids(spec, ss.d)
+    ids = slice_ids(spec, ss.d, name)
     terms = oracle.vertex_terms(tn, tree)
     root = tree.root
     a, b = tree.children(root)

@@ -12,8 +12,9 @@ arithmetic, for the sum over the fixture's slices, and for the full d24
 amplitude.  Slices that are exactly zero in exact arithmetic (about half of
 this circuit's slices: a sliced CZ bond projects a |0> input onto |1>) come out
 of the complex128 oracle as ~1e-16 of the nonzero slices' magnitude and have no
-relative error; for them the test asserts |c_gpu| stays below 1e-12 of the
-largest slice of the set.  Each slice's condition ||x_root|| ||y_root|| / |c|
+relative error (the GPU's complex64 round-off of them is ~1e-8 of the nonzero
+slices, the oracle's complex128 one ~1e-16); for them the test asserts |c_gpu|
+stays below 1e-7 of the largest slice of the set.  Each slice's condition ||x_root|| ||y_root|| / |c|
 is printed beside its error.
 """
 import json
@@ -70,7 +71,7 @@ def test_northstar_slices(key):
     lines, worst = [], 0.0
     for row, g, r in zip(fx["slices"], got, refs):
         if abs(r) <= 1e-10 * big:  # zero in exact arithmetic
-            assert abs(g) <= 1e-12 * big, (row["slice"], g, r)
+            assert abs(g) <= 1e-7 * big, (row["slice"], g, r)
             lines.append(f"slice {row['slice']}: exact zero (|gpu| {abs(g) / big:.1e} of max)")
             continue
         rel = abs(g - r) / abs(r)
