@@ -471,6 +471,10 @@ def main():
                 best = (t, mhz, pms, cg)
         probe = {"tf32_tflops": best[0], "sm_mhz": best[1], "ms": best[2], "cta_group": best[3],
                  "tf32_flop_per_clk_per_sm": best[0] * 1e12 / (best[1] * 1e6) / sms}
+        _native.mma_peak("ffma", 1, 20000, stream.cuda_stream)
+        f_t, f_mhz, _ = _native.mma_peak("ffma", 1, 200000, stream.cuda_stream)
+        probe.update({"ffma_tflops": f_t, "ffma_sm_mhz": f_mhz,
+                      "ffma_flop_per_clk_per_sm": f_t * 1e12 / (f_mhz * 1e6) / sms})
     committed, committed_src = load_mma_peak()
     if probe and clocks.get("sm_mhz"):
         # the probe's per-clock rate at the clock the timed slices ran at (the
@@ -530,6 +534,27 @@ def main():
                                  "frac": bb / (bt / 1e3) / 1e9 / peaks["hbm_gbs"]}
     small = [b for k, v, t, b in prof_b if (k == "pack" or (k == "simt" and b > 0)) and b < 16e6]
     hbm["small_launches"] = {"count": len(small), "median_bytes": float(np.median(small)) if small else None}
+    # slice roofline: t*_v = max(8 U_v / P, 8 B x (|A|+|B|+|O|) / BW) per
+    # per-slice vertex -- P = the split-TF32 ceiling for tensor-core vertices, the
+    # FFMA ceiling (same clock) for SIMT ones -- summed and divided by the
+    # measured slice time
+    p_simt = (probe["ffma_flop_per_clk_per_sm"] * sms * clocks["sm_mhz"] * 1e6 / 1e12
+              if probe and clocks.get("sm_mhz") else None)
+    t_star = 0.0
+    if p_simt:
+        bw = peaks["hbm_gbs"] * 1e9
+        for x in info.values():
+            if x["hoisted"]:
+                continue
+            byts = 8.0 * x["batch"] * (x["m"] * x["k"] + x["n"] * x["k"] + x["m"] * x["n"])
+            pk = p_c if x["kind"] == "gemm_tc" else p_simt
+            t_star += max(8.0 * x["macs"] / (pk * 1e12), byts / bw)
+    slice_roofline = {"t_star_ms": 1e3 * t_star, "slice_ms": slice_ms,
+                      "frac": 1e3 * t_star / slice_ms if slice_ms and t_star else None,
+                      "p_simt_tflops": p_simt,
+                      "def": "sum over per-slice vertices of max(8 U_v / P, 8 B (|A|+|B|+|O|) / HBM BW) "
+                             "/ profiled slice time (P: split-TF32 ceiling for tensor-core vertices, "
+                             "FFMA ceiling for SIMT vertices, both at the timed clock)"}
     by_kind = {}
     for k, v, t in prof:
         by_kind[k] = by_kind.get(k, 0.0) + t
@@ -552,7 +577,8 @@ def main():
                 "nominal_peak": NOMINAL_TF32 / 3.0,
                 "frac_nominal": achieved / (NOMINAL_TF32 / 3.0),
                 "dominant_min_frac_nominal": min((d["tflops"] / (NOMINAL_TF32 / 3.0) for d in dom), default=None),
-                "hbm_bound_kernels": hbm}
+                "hbm_bound_kernels": hbm,
+                "slice_roofline": slice_roofline}
     if args.profile_out and rank == 0:
         with open(args.profile_out, "w") as fh:
             json.dump({"launches": prof, "vertices": list(info.values())}, fh, default=str)

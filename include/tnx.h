@@ -196,7 +196,9 @@ int tnx_gemm_c64(const void* A, const void* B, void* C, int64_t batch, int64_t M
  * operands, one CTA per SM, no TMA / promotion / epilogue.  kind 0 =
  * kind::tf32 (K=8), 1 = kind::f16 with BF16 operands (K=16).  Returns dense
  * TFLOP/s over the device (2*M*N*K per MMA), the median SM clock the CTAs
- * measured (clock64 / globaltimer) and the event-timed duration. */
+ * measured (clock64 / globaltimer) and the event-timed duration.  kind 2 is
+ * the FP32 SIMT ceiling instead: 8 independent FFMA chains per thread,
+ * 4 x 256 threads per SM (cta_group ignored; 16 flop per thread-iteration). */
 int tnx_mma_peak(int32_t kind, int32_t cta_group, int64_t iters, void* stream, double* tflops,
                  double* sm_mhz, double* ms);
 

@@ -127,6 +127,6 @@ def mma_peak(kind="tf32", cta_group=2, iters=200000, stream=None):
     """Tensor-pipe ceiling measured by ``tnx_mma_peak``: (TFLOP/s, SM MHz, ms)."""
     lib = load()
     t, m, ms = C.c_double(), C.c_double(), C.c_double()
-    check(lib.tnx_mma_peak({"tf32": 0, "bf16": 1}[kind], cta_group, iters, stream, C.byref(t), C.byref(m),
+    check(lib.tnx_mma_peak({"tf32": 0, "bf16": 1, "ffma": 2}[kind], cta_group, iters, stream, C.byref(t), C.byref(m),
                            C.byref(ms)))
     return t.value, m.value, ms.value

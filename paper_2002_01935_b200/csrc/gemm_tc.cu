@@ -663,7 +663,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // partial).  Promotion adds S (1 + that) -- an unbiased estimate, so the
         // residual error is the zero-mean part that grows like sqrt(n).
         const int nkb_r = r == 0 ? F : min(nkb - F - (r - 1) * P, P);
-        const float delta = g.rz_kappa * 5.9604645e-8f * (float)(6 * nkb_r - 2);
+        // (mixed TF32/BF16 mode: 8 MMAs per k-block -- two BF16 cross-term MMAs,
+        // then the two TF32 hi*hi ones, per k-step -- giving 4 n_kb - 1)
+        const float delta = g.rz_kappa * 5.9604645e-8f * (float)(MIX ? 4 * nkb_r - 1 : 6 * nkb_r - 2);
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           uint32_t re[32], im[32];
@@ -997,10 +999,9 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
     // truncations lose bits).  0.35 removes the circuits' bias and 60 % of the
     // random-data bias; on data whose sums are all exact it over-corrects by
     // at most 0.35 * 2^-24 * (6 n_kb - 2) per GEMM (< 7.1e-7 for a 6-k-block
-    // round), below the uncompensated bias on random data.  The mixed TF32/BF16
-    // mode has another MMA sequence and is not compensated.
+    // round), below the uncompensated bias on random data.
     static const float kappa = getenv("TNX_GEMM_RZC") ? (float)atof(getenv("TNX_GEMM_RZC")) : 0.35f;
-    a.rz_kappa = g.mix ? 0.0f : kappa;
+    a.rz_kappa = kappa;
   }
   const int splits = g.splits > 1 ? g.splits : 1;
   a.kb_per_split = (a.num_kb + splits - 1) / splits;
@@ -1173,6 +1174,31 @@ __global__ void __launch_bounds__(PEAK_THREADS, 1)
   }
 }
 
+// FP32 SIMT ceiling: 8 independent FFMA chains per thread, 4 x 256 threads per
+// SM; the result is folded into rec so the chains are live.
+__global__ void __launch_bounds__(256) ffma_peak_kernel(int64_t iters, unsigned long long* rec) {
+  float a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = 1.0f + 1e-7f * (float)(threadIdx.x + j);
+  const float b = 0.999999f, c = 1e-7f;
+  unsigned long long c0 = clock64(), g0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+  for (int64_t i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = fmaf(a[j], b, c);
+  }
+  float acc = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc += a[j];
+  const unsigned long long c1 = clock64();
+  unsigned long long g1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+  if (threadIdx.x == 0 && (blockIdx.x & 3) == 0) {
+    rec[2 * (blockIdx.x >> 2)] = (c1 - c0) + (acc == 12345.f ? 1ull : 0ull);
+    rec[2 * (blockIdx.x >> 2) + 1] = g1 - g0;
+  }
+}
+
 template <bool TWO_SM, bool BF16>
 cudaError_t launch_mma_peak(int64_t iters, unsigned long long* rec, int grid, cudaStream_t st) {
   auto k = mma_peak_kernel<TWO_SM, BF16>;
@@ -1195,18 +1221,24 @@ cudaError_t launch_mma_peak(int64_t iters, unsigned long long* rec, int grid, cu
 }
 }  // namespace
 
-int gemm_mma_peak(int bf16, int two_sm, int64_t iters, cudaStream_t st, double* tflops, double* sm_mhz,
+int gemm_mma_peak(int kind, int two_sm, int64_t iters, cudaStream_t st, double* tflops, double* sm_mhz,
                   double* ms, char* err, size_t errlen) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = two_sm ? (sms / 2) * 2 : sms;
+  const bool ffma = kind == 2;
+  const int bf16 = kind == 1;
+  const int grid = ffma ? sms : two_sm ? (sms / 2) * 2 : sms;
   unsigned long long* rec = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   cudaError_t e = cudaMalloc(&rec, sizeof(unsigned long long) * 2 * grid);
   if (e == cudaSuccess) e = cudaEventCreate(&e0);
   if (e == cudaSuccess) e = cudaEventCreate(&e1);
   auto launch = [&](int64_t n) {
+    if (ffma) {
+      ffma_peak_kernel<<<4 * sms, 256, 0, st>>>(n, rec);
+      return cudaGetLastError();
+    }
     if (two_sm) return bf16 ? launch_mma_peak<true, true>(n, rec, grid, st) : launch_mma_peak<true, false>(n, rec, grid, st);
     return bf16 ? launch_mma_peak<false, true>(n, rec, grid, st) : launch_mma_peak<false, false>(n, rec, grid, st);
   };
@@ -1226,8 +1258,10 @@ int gemm_mma_peak(int bf16, int two_sm, int64_t iters, cudaStream_t st, double* 
     snprintf(err, errlen, "mma peak: %s", cudaGetErrorString(e));
     return 1;
   }
-  // flop per MMA per CTA: 2 * 128 rows * 256 columns * K (8 tf32 / 16 bf16)
-  const double flop = (double)grid * (double)iters * 2.0 * BM * 2 * BN * (bf16 ? 16 : 8);
+  // flop per MMA per CTA: 2 * 128 rows * 256 columns * K (8 tf32 / 16 bf16);
+  // FFMA: 2 flop x 8 chains per thread per iteration, 4 x 256 threads per SM
+  const double flop = ffma ? (double)sms * 1024.0 * (double)iters * 16.0
+                           : (double)grid * (double)iters * 2.0 * BM * 2 * BN * (bf16 ? 16 : 8);
   *ms = t;
   *tflops = flop / (t * 1e-3) / 1e12;
   std::vector<double> mhz;

@@ -1825,8 +1825,8 @@ int tnx_gemm_c64(const void* A, const void* B, void* C, int64_t batch, int64_t M
 
 int tnx_mma_peak(int32_t kind, int32_t cta_group, int64_t iters, void* stream, double* tflops,
                  double* sm_mhz, double* ms) {
-  if ((kind != 0 && kind != 1) || (cta_group != 1 && cta_group != 2) || iters < 8 || !tflops || !sm_mhz || !ms)
-    return fail(TNX_ERR_INVALID, "tnx_mma_peak: kind 0 (tf32) / 1 (bf16), cta_group 1 / 2, iters >= 8");
+  if (kind < 0 || kind > 2 || (cta_group != 1 && cta_group != 2) || iters < 8 || !tflops || !sm_mhz || !ms)
+    return fail(TNX_ERR_INVALID, "tnx_mma_peak: kind 0 (tf32) / 1 (bf16) / 2 (ffma), cta_group 1 / 2, iters >= 8");
   char ebuf[256];
   if (gemm_mma_peak(kind, cta_group == 2, iters, static_cast<cudaStream_t>(stream), tflops, sm_mhz, ms, ebuf,
                     sizeof(ebuf)))

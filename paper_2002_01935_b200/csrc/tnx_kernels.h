@@ -260,8 +260,9 @@ int gemm_stack_enabled();
 int gemm_use_stack(int64_t batch, int64_t M, int64_t N, int64_t kp, int two_sm);
 cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st);
 int gemm_init_attributes(char* err, size_t errlen);
-// MMA-only tensor-pipe ceiling (no TMA / epilogue): TFLOP/s, median SM MHz
-int gemm_mma_peak(int bf16, int two_sm, int64_t iters, cudaStream_t st, double* tflops, double* sm_mhz,
+// MMA-only tensor-pipe ceiling (no TMA / epilogue; kind 0 tf32, 1 bf16) or the
+// FP32 FFMA ceiling (kind 2): TFLOP/s, median SM MHz
+int gemm_mma_peak(int kind, int two_sm, int64_t iters, cudaStream_t st, double* tflops, double* sm_mhz,
                   double* ms, char* err, size_t errlen);
 
 }  // namespace tnx

@@ -25,14 +25,15 @@ def main():
     b = torch.randn(1, N, K, dtype=torch.complex64, device="cuda", generator=g)
     c = torch.empty(1, M, N, dtype=torch.complex64, device="cuda")
     s = torch.cuda.Stream()
-    nat.check(lib.tnx_gemm_c64(a.data_ptr(), b.data_ptr(), c.data_ptr(), 1, M, N, K, 1, s.cuda_stream))
+    prec = int(os.environ.get("PREC", "1"))  # 1 = 3xtf32, 2 = tf32-bf16x
+    nat.check(lib.tnx_gemm_c64(a.data_ptr(), b.data_ptr(), c.data_ptr(), 1, M, N, K, prec, s.cuda_stream))
     torch.cuda.synchronize()
     ref = torch.einsum("bmk,bnk->bmn", a.to(torch.complex128), b.to(torch.complex128))
     d = c.to(torch.complex128) - ref
     rr = (ref.abs() ** 2).sum().item()
     bias = (ref.conj() * d).sum().real.item() / rr
     resid = (d - bias * ref).norm().item() / ref.norm().item()
-    out = {"M": M, "N": N, "K": K, "env": {k: v for k, v in os.environ.items() if k.startswith("TNX_")},
+    out = {"M": M, "N": N, "K": K, "prec": prec, "env": {k: v for k, v in os.environ.items() if k.startswith("TNX_")},
            "bias": bias, "resid": resid, "err": d.norm().item() / ref.norm().item()}
     print(json.dumps(out))
 

@@ -36,6 +36,12 @@ def main():
             rows.append({"kind": kind, "cta_group": cg, "mode": "burst", "iters": it, "ms": ms,
                          "tflops": t, "sm_mhz": mhz, "flop_per_clk_per_sm": t * 1e12 / (mhz * 1e6) / sms})
             print(json.dumps(rows[-1]), flush=True)
+    t, mhz, ms = _native.mma_peak("ffma", 1, 20000)
+    it = max(1000, int(20000 * 50.0 / max(ms, 1e-3)))
+    t, mhz, ms = _native.mma_peak("ffma", 1, it)
+    rows.append({"kind": "ffma", "cta_group": 0, "mode": "burst", "iters": it, "ms": ms, "tflops": t,
+                 "sm_mhz": mhz, "flop_per_clk_per_sm": t * 1e12 / (mhz * 1e6) / sms})
+    print(json.dumps(rows[-1]), flush=True)
     if args.sustained_s > 0:
         for kind in ("tf32",):
             for cg in (2,):
@@ -48,7 +54,8 @@ def main():
     best = max((r for r in rows if r["kind"] == "tf32" and r["mode"] == "burst"), key=lambda r: r["tflops"])
     summary = {"device": torch.cuda.get_device_name(0), "sms": sms, "rows": rows,
                "tf32_peak_tflops": best["tflops"], "tf32_peak_sm_mhz": best["sm_mhz"],
-               "complex_3xtf32_peak_tflops": best["tflops"] / 3.0}
+               "complex_3xtf32_peak_tflops": best["tflops"] / 3.0,
+               "ffma_tflops": rows[4]["tflops"] if len(rows) > 4 else None}
     print(json.dumps({k: v for k, v in summary.items() if k != "rows"}))
     if args.out:
         with open(args.out, "w") as fh:
