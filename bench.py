@@ -200,7 +200,9 @@ def run_reference(args):
     ids = list(range(warm + steps))
     if args.slices == "nonzero" and os.path.exists(nz_path):
         with open(nz_path) as fh:
-            ids = [int(x) for x in json.load(fh)["ids"]][:warm + steps]  # the b200 arm's rank-0 ids
+            nz_rec = json.load(fh)
+        if float(nz_rec["ws"]) == float(ss.Ws) and str(nz_rec.get("d", ss.d)) == str(ss.d):
+            ids = [int(x) for x in nz_rec["ids"]][:warm + steps]  # the b200 arm's rank-0 ids
     for i in range(len(ids)):
         val, ops, dt, cores, _ = cpu_baseline(tn, tree, ss, ids[i], budget)
         assert ops == per_slice
@@ -318,8 +320,9 @@ def main():
         with open(nz_path) as fh:
             nz_rec = json.load(fh)
         nz_ids = [int(x) for x in nz_rec["ids"]]
-    elif (W + K) * world * 2 > plan.d:
-        raise SystemExit("slice prefix larger than d_sliced")
+        # the list belongs to one slice set (the workload's default W_s)
+        use_list = float(nz_rec["ws"]) == float(ss.Ws) and str(nz_rec.get("d", ss.d)) == str(ss.d)
+    cyc = (not use_list) and (W + K) * world > plan.d  # few slices (or unsliced): repeat them
     # an explicit stream: the legacy default stream has handle 0, which the C
     # ABI reads as "the library's own stream"
     stream = torch.cuda.Stream()
@@ -331,11 +334,13 @@ def main():
     # draw less power); rank r takes the r-th block of W+K ids, cycling
     # through the list.  "prefix": the prefix [0, world*(W+K)) of the slice
     # enumeration, one contiguous block per rank (bit-exact sub-range).
-    base, _ = slice_range(0, world * (W + K), world, rank)
+    base = slice_range(0, world * (W + K), world, rank)[0] if not cyc else rank * (W + K)
 
     def job_ids(offset, n):
         if use_list:
             return [nz_ids[(offset + i) % len(nz_ids)] for i in range(n)]
+        if cyc:
+            return [(offset + i) % plan.d for i in range(n)]
         return list(range(offset, offset + n))
 
     warm_ids = job_ids(rank * (W + K) if use_list else base, W)
@@ -370,14 +375,21 @@ def main():
     clk = ClockSampler(local).start()
     barrier()
     torch.cuda.synchronize()
+    from paper_2002_01935_b200 import _native
+    stamps = _native.ClockStamps()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    stamps.start(stream.cuda_stream)
     e0.record(stream)
     run_ids(timed_ids)
     e1.record(stream)
+    stamps.stop(stream.cuda_stream)
     torch.cuda.synchronize()
     barrier()
     clocks = clk.stop()
+    # mean SM clock over the timed slices from the SMs' own cycle counters
+    # (clock64 / globaltimer stamps on the stream before and after)
+    clocks["sm_mhz_cycles"], clocks["sm_cycle_stamps"] = stamps.mhz()
     ms = e0.elapsed_time(e1)
     t_max = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if use_dist:
@@ -418,19 +430,22 @@ def main():
         n_s = max(K, int(math.ceil(args.sustained_s * 1e3 / (ms_max / K))))
         s_base = world * (W + K) + rank * n_s
         sus_ids = job_ids(s_base, n_s)
-        if use_list or s_base + n_s <= plan.d:
+        if use_list or cyc or s_base + n_s <= plan.d:
             plan.reset(stream)
             clk2 = ClockSampler(local).start()
             barrier()
             torch.cuda.synchronize()
             f0 = torch.cuda.Event(enable_timing=True)
             f1 = torch.cuda.Event(enable_timing=True)
+            stamps.start(stream.cuda_stream)
             f0.record(stream)
             run_ids(sus_ids)
             f1.record(stream)
+            stamps.stop(stream.cuda_stream)
             torch.cuda.synchronize()
             barrier()
             clocks2 = clk2.stop()
+            clocks2["sm_mhz_cycles"], clocks2["sm_cycle_stamps"] = stamps.mhz()
             ms2 = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=red_dev)
             if use_dist:
                 dist.all_reduce(ms2, op=dist.ReduceOp.MAX)
@@ -459,7 +474,6 @@ def main():
     # MMA-only tcgen05.mma kind::tf32 loop (tnx_mma_peak: no TMA, no epilogue,
     # operands resident in shared memory, one CTA pair per SM pair), divided
     # by 3 (split-TF32: 24 M N K real tensor flop per 8 M N K complex flop).
-    from paper_2002_01935_b200 import _native
     probe = None
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     if not args.no_tf32_probe:
@@ -476,15 +490,16 @@ def main():
         probe.update({"ffma_tflops": f_t, "ffma_sm_mhz": f_mhz,
                       "ffma_flop_per_clk_per_sm": f_t * 1e12 / (f_mhz * 1e6) / sms})
     committed, committed_src = load_mma_peak()
-    if probe and clocks.get("sm_mhz"):
+    timed_mhz = clocks.get("sm_mhz_cycles") or clocks.get("sm_mhz")
+    if probe and timed_mhz:
         # the probe's per-clock rate at the clock the timed slices ran at (the
         # MMA-only loop on random operands draws more power than the GEMM and
         # runs at a lower clock, so its raw TFLOP/s would understate the ceiling)
-        p_c = probe["tf32_flop_per_clk_per_sm"] * sms * clocks["sm_mhz"] * 1e6 / 1e12 / 3.0
+        p_c = probe["tf32_flop_per_clk_per_sm"] * sms * timed_mhz * 1e6 / 1e12 / 3.0
         peak_src = (f"live tnx_mma_peak (tcgen05.mma kind::tf32 MMA-only loop, cta_group::{probe['cta_group']}): "
-                    f"{probe['tf32_flop_per_clk_per_sm']:.0f} flop/clk/SM x {sms} SMs x {clocks['sm_mhz']:.0f} MHz "
-                    f"(median SM clock sampled during the timed slices) / 3 split-TF32 passes; raw probe "
-                    f"{probe['tf32_tflops']:.1f} TFLOP/s at {probe['sm_mhz']:.0f} MHz")
+                    f"{probe['tf32_flop_per_clk_per_sm']:.0f} flop/clk/SM x {sms} SMs x {timed_mhz:.0f} MHz "
+                    f"(mean SM clock over the timed slices, from clock64/globaltimer stamps) / 3 split-TF32 "
+                    f"passes; raw probe {probe['tf32_tflops']:.1f} TFLOP/s at {probe['sm_mhz']:.0f} MHz")
     elif probe:
         p_c = probe["tf32_tflops"] / 3.0
         peak_src = (f"live tnx_mma_peak: tcgen05.mma kind::tf32 MMA-only loop, cta_group::{probe['cta_group']}, "
@@ -538,8 +553,8 @@ def main():
     # per-slice vertex -- P = the split-TF32 ceiling for tensor-core vertices, the
     # FFMA ceiling (same clock) for SIMT ones -- summed and divided by the
     # measured slice time
-    p_simt = (probe["ffma_flop_per_clk_per_sm"] * sms * clocks["sm_mhz"] * 1e6 / 1e12
-              if probe and clocks.get("sm_mhz") else None)
+    p_simt = (probe["ffma_flop_per_clk_per_sm"] * sms * timed_mhz * 1e6 / 1e12
+              if probe and timed_mhz else None)
     t_star = 0.0
     if p_simt:
         bw = peaks["hbm_gbs"] * 1e9
@@ -644,7 +659,9 @@ def main():
                            "slices": (f"nonzero slice ids ({len(nz_ids)} in benchdata/{args.config}.slices.json, "
                                       f"nonzero fraction of a random sample {nz_rec['nonzero_fraction']:.3f}); "
                                       f"rank r times ids [r*(W+K)+W, (r+1)*(W+K)) of the list, cyclic"
-                                      if use_list else f"prefix [0, {world * (W + K)}) of the enumeration"),
+                                      if use_list else (f"slice ids cycling through all {plan.d} slices"
+                                                        if cyc else
+                                                        f"prefix [0, {world * (W + K)}) of the enumeration")),
                            "tree_source": meta["tree_source"], "precision": args.precision,
                            "ws_auto": meta.get("ws_auto")},
                 "slices_per_s": slices_per_s,

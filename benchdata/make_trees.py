@@ -31,8 +31,12 @@ from hypertn.drivers import greedy as rgreedy  # noqa: E402
 from paper_2002_01935_b200.harness import generators as gen  # noqa: E402
 
 CONFIGS = {
+    "cfg1_3reg50": (lambda: gen.random_regular(50, 3, seed=0), 32, True),
     "cfg2_5reg100": (lambda: gen.random_regular(100, 5, seed=0), 48, False),
     "cfg3_lattice20": (lambda: gen.square_lattice(20, seed=0), 24, True),
+    # BASELINE configs[2] "greedy vs hyper tree": the plain greedy tree
+    # (greedy_sample alpha=1, tau=0, seed 0) next to cfg3's best-of search
+    "cfg3g_lattice20": (lambda: gen.square_lattice(20, seed=0), 0, False),
     # min-fill varies a lot with its seed on this network (log10 C 23.4-28.0 over
     # 200 seeds; greedy's best of 49 shots is 26.0), so cfg4 samples 200 seeds
     "cfg4_7x7_d40": (lambda: gen.grid_circuit(7, 7, 40, seed=0), 48, 200),

@@ -202,6 +202,12 @@ int tnx_gemm_c64(const void* A, const void* B, void* C, int64_t batch, int64_t M
 int tnx_mma_peak(int32_t kind, int32_t cta_group, int64_t iters, void* stream, double* tflops,
                  double* sm_mhz, double* ms);
 
+/* Measurement: `blocks` one-warp blocks each write (SM id, clock64,
+ * globaltimer ns) to device_out[3*b .. 3*b+2] on `stream`.  Two stamps around
+ * a timed region give, per SM, cycles / ns = the mean SM clock over the region
+ * (used by bench.py to price the roofline at the clock the kernels ran at). */
+int tnx_clock_stamp(uint64_t* device_out, int32_t blocks, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -78,6 +78,7 @@ SIGNATURES = {
                                     C.POINTER(C.c_int32)]),
     "tnx_gemm_c64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
                                C.c_int64, C.c_int32, C.c_void_p]),
+    "tnx_clock_stamp": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
     "tnx_mma_peak": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_void_p, C.POINTER(C.c_double),
                                C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }
@@ -130,3 +131,33 @@ def mma_peak(kind="tf32", cta_group=2, iters=200000, stream=None):
     check(lib.tnx_mma_peak({"tf32": 0, "bf16": 1, "ffma": 2}[kind], cta_group, iters, stream, C.byref(t), C.byref(m),
                            C.byref(ms)))
     return t.value, m.value, ms.value
+
+
+class ClockStamps:
+    """Mean SM clock over a region of a stream: ``start(stream)`` ...
+    ``stop(stream)``, then ``mhz()`` after the stream has synchronised.  Each
+    stamp launches ``blocks`` one-warp blocks recording (SM id, clock64,
+    globaltimer); SMs seen in both stamps give cycles / ns."""
+
+    def __init__(self, blocks=592):
+        import torch
+        self.blocks = blocks
+        self.buf = torch.zeros((2, 3 * blocks), dtype=torch.int64, device="cuda")
+
+    def _stamp(self, i, stream):
+        check(load().tnx_clock_stamp(self.buf[i].data_ptr(), self.blocks, stream))
+
+    def start(self, stream):
+        self._stamp(0, stream)
+
+    def stop(self, stream):
+        self._stamp(1, stream)
+
+    def mhz(self):
+        a = self.buf.cpu().numpy().reshape(2, self.blocks, 3)
+        first = {int(r[0]): (int(r[1]), int(r[2])) for r in a[0]}
+        last = {int(r[0]): (int(r[1]), int(r[2])) for r in a[1]}
+        rates = [(last[k][0] - first[k][0]) / (last[k][1] - first[k][1]) * 1e3
+                 for k in first if k in last and last[k][1] > first[k][1]]
+        rates.sort()
+        return rates[len(rates) // 2] if rates else None, len(rates)

@@ -75,12 +75,23 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
 }
 
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* tmap, uint32_t mbar, int c0,
-                                            int c1, int c2) {
+                                            int c1, int c2, uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(mbar), "r"(c0), "r"(c1), "r"(c2)
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(mbar), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
       : "memory");
+}
+
+// L2 policy of the operand loads: evict_last (operands are re-read by the other
+// tiles of the wave) or evict_normal (TNX_GEMM_L2HINT=0)
+__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+  uint64_t p;
+  if (keep)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 
 // UMMA shared-memory descriptor: K-major, SWIZZLE_64B, rows of 64 B,
@@ -170,6 +181,8 @@ struct GemmArgs {
   int32_t ksnake;        // odd waves traverse K in reverse (L2 reuse across waves)
   int32_t first;         // k-blocks of a unit's first TMEM round (>= promote; see launch_gemm)
   float rz_kappa;        // round-toward-zero compensation (see the promotion loop); 0 disables
+  int32_t l2keep;        // operand loads with an L2 evict_last policy (TNX_GEMM_L2HINT bit 0)
+  int32_t stcs;          // results stored evict-first (bit 1)
 };
 
 __device__ __forceinline__ int64_t map_offset(const IdxMap& m, int64_t idx) {
@@ -188,6 +201,15 @@ __device__ __forceinline__ int64_t map_offset(const IdxMap& m, int64_t idx) {
     o += r * m.st0[i];
   }
   return o;
+}
+
+// result stores: plain, or streaming (st.global.cs, evict-first) with
+// TNX_GEMM_L2HINT bit 1
+__device__ __forceinline__ void st_res(float4* p, float4 v, bool cs) {
+  if (cs) __stcs(p, v); else *p = v;
+}
+__device__ __forceinline__ void st_res(float* p, float v, bool cs) {
+  if (cs) __stcs(p, v); else *p = v;
 }
 
 // Epilogue store of one thread's 64 promoted columns of row `row` (global
@@ -228,13 +250,13 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& g, float2* out, i
           rl[t] = tf32_lo(mre[j + t], rh[t]);
           il[t] = tf32_lo(mim[j + t], ih[t]);
         }
-        *reinterpret_cast<float4*>(d + off) = make_float4(rh[0], rh[1], rh[2], rh[3]);
-        *reinterpret_cast<float4*>(d + off + ps) = make_float4(rl[0], rl[1], rl[2], rl[3]);
-        *reinterpret_cast<float4*>(d + off + 2 * ps) = make_float4(ih[0], ih[1], ih[2], ih[3]);
-        *reinterpret_cast<float4*>(d + off + 3 * ps) = make_float4(il[0], il[1], il[2], il[3]);
+        st_res(reinterpret_cast<float4*>(d + off), make_float4(rh[0], rh[1], rh[2], rh[3]), g.stcs);
+        st_res(reinterpret_cast<float4*>(d + off + ps), make_float4(rl[0], rl[1], rl[2], rl[3]), g.stcs);
+        st_res(reinterpret_cast<float4*>(d + off + 2 * ps), make_float4(ih[0], ih[1], ih[2], ih[3]), g.stcs);
+        st_res(reinterpret_cast<float4*>(d + off + 3 * ps), make_float4(il[0], il[1], il[2], il[3]), g.stcs);
         if (g.dstack) {
-          *reinterpret_cast<float4*>(d + off + 4 * ps) = make_float4(-ih[0], -ih[1], -ih[2], -ih[3]);
-          *reinterpret_cast<float4*>(d + off + 5 * ps) = make_float4(-il[0], -il[1], -il[2], -il[3]);
+          st_res(reinterpret_cast<float4*>(d + off + 4 * ps), make_float4(-ih[0], -ih[1], -ih[2], -ih[3]), g.stcs);
+          st_res(reinterpret_cast<float4*>(d + off + 5 * ps), make_float4(-il[0], -il[1], -il[2], -il[3]), g.stcs);
         }
       }
     }
@@ -251,18 +273,18 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& g, float2* out, i
       const float re = mre[j], im = mim[j];
       const float rh = tf32_hi(re);
       const float ih = tf32_hi(im);
-      d[off] = rh;
-      d[off + 2 * ps] = ih;
+      st_res(d + off, rh, g.stcs);
+      st_res(d + off + 2 * ps, ih, g.stcs);
       if constexpr (MIX) {
         store_mix_x(d + ps, off, re, g.dside);
         store_mix_x(d + 3 * ps, off, im, g.dside);
       } else {
         const float il = tf32_lo(im, ih);
-        d[off + ps] = tf32_lo(re, rh);
-        d[off + 3 * ps] = il;
+        st_res(d + off + ps, tf32_lo(re, rh), g.stcs);
+        st_res(d + off + 3 * ps, il, g.stcs);
         if (g.dstack) {
-          d[off + 4 * ps] = -ih;
-          d[off + 5 * ps] = -il;
+          st_res(d + off + 4 * ps, -ih, g.stcs);
+          st_res(d + off + 5 * ps, -il, g.stcs);
         }
       }
     }
@@ -273,7 +295,7 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& g, float2* out, i
     float4* dst = reinterpret_cast<float4*>(orow + col0);
 #pragma unroll
     for (int j = 0; j < 32; ++j)
-      dst[j] = make_float4(mre[2 * j], mim[2 * j], mre[2 * j + 1], mim[2 * j + 1]);
+      st_res(dst + j, make_float4(mre[2 * j], mim[2 * j], mre[2 * j + 1], mim[2 * j + 1]), g.stcs);
   } else {
 #pragma unroll
     for (int j = 0; j < 64; ++j)
@@ -341,11 +363,11 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void tma_load_3d_2sm(uint32_t dst, const void* tmap, uint32_t mbar, int c0, int c1,
-                                                int c2) {
+                                                int c2, uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(mbar & PEER_MASK), "r"(c0), "r"(c1), "r"(c2)
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(mbar & PEER_MASK), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
       : "memory");
 }
 __device__ __forceinline__ void umma_tf32_2sm(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
@@ -460,6 +482,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
+      const uint64_t pol = l2_policy(g.l2keep != 0);
       int stage = 0;
       uint32_t phase = 0;
       for (int u = cid; u < units; u += ncta) {
@@ -491,17 +514,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if constexpr (STACK) {
               // B slot p of this CTA: CTA0 planes {0, 1, 4, 5}, CTA1 {2, 3, 0, 1}
               const int bp = rank == 0 ? (p < 2 ? p : p + 2) : (p < 2 ? p + 2 : p - 2);
-              tma_load_3d_2sm(smem_addr(sbase + p * C::A_BYTES), &tm_a, fb, 0, row_a, p * g.num_kb + kbg);
+              tma_load_3d_2sm(smem_addr(sbase + p * C::A_BYTES), &tm_a, fb, 0, row_a, p * g.num_kb + kbg, pol);
               tma_load_3d_2sm(smem_addr(sbase + 4 * C::A_BYTES + p * C::B_BYTES), &tm_b, fb, 0, row_b,
-                              bp * g.num_kb + kbg);
+                              bp * g.num_kb + kbg, pol);
             } else if constexpr (TWO_SM) {
-              tma_load_3d_2sm(smem_addr(sbase + p * C::A_BYTES), &tm_a, fb, 0, row_a, p * g.num_kb + kbg);
+              tma_load_3d_2sm(smem_addr(sbase + p * C::A_BYTES), &tm_a, fb, 0, row_a, p * g.num_kb + kbg, pol);
               tma_load_3d_2sm(smem_addr(sbase + 4 * C::A_BYTES + p * C::B_BYTES), &tm_b, fb, 0, row_b,
-                              p * g.num_kb + kbg);
+                              p * g.num_kb + kbg, pol);
             } else {
-              tma_load_3d(smem_addr(sbase + p * C::A_BYTES), &tm_a, fb, 0, row_a, p * g.num_kb + kbg);
+              tma_load_3d(smem_addr(sbase + p * C::A_BYTES), &tm_a, fb, 0, row_a, p * g.num_kb + kbg, pol);
               tma_load_3d(smem_addr(sbase + 4 * C::A_BYTES + p * C::B_BYTES), &tm_b, fb, 0, row_b,
-                          p * g.num_kb + kbg);
+                          p * g.num_kb + kbg, pol);
             }
           }
           if (++stage == C::NSTAGE) {
@@ -1002,6 +1025,9 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
     // round), below the uncompensated bias on random data.
     static const float kappa = getenv("TNX_GEMM_RZC") ? (float)atof(getenv("TNX_GEMM_RZC")) : 0.35f;
     a.rz_kappa = kappa;
+    static const int l2hint = getenv("TNX_GEMM_L2HINT") ? atoi(getenv("TNX_GEMM_L2HINT")) : 1;
+    a.l2keep = l2hint & 1;
+    a.stcs = (l2hint >> 1) & 1;
   }
   const int splits = g.splits > 1 ? g.splits : 1;
   a.kb_per_split = (a.num_kb + splits - 1) / splits;

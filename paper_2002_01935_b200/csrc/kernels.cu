@@ -840,6 +840,25 @@ cudaError_t launch_set_counter(unsigned long long* counter, unsigned long long v
   return cudaGetLastError();
 }
 
+// Clock stamps for measurement: every block records (SM id, clock64,
+// globaltimer).  Two stamps bracketing a timed region give each SM's cycle
+// count over the region and hence the mean SM clock it ran at.
+__global__ void clock_stamp_kernel(unsigned long long* out) {
+  if (threadIdx.x != 0) return;
+  unsigned int smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  unsigned long long gt;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+  out[3 * blockIdx.x] = smid;
+  out[3 * blockIdx.x + 1] = clock64();
+  out[3 * blockIdx.x + 2] = gt;
+}
+
+cudaError_t launch_clock_stamp(unsigned long long* out, int blocks, cudaStream_t st) {
+  clock_stamp_kernel<<<blocks, 32, 0, st>>>(out);
+  return cudaGetLastError();
+}
+
 __global__ void convert_kernel(const double2* __restrict__ s, float2* __restrict__ d, int64_t n) {
   pdl_wait();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;

@@ -1834,4 +1834,12 @@ int tnx_mma_peak(int32_t kind, int32_t cta_group, int64_t iters, void* stream, d
   return TNX_OK;
 }
 
+int tnx_clock_stamp(uint64_t* device_out, int32_t blocks, void* stream) {
+  if (!device_out || blocks < 1) return fail(TNX_ERR_INVALID, "tnx_clock_stamp: need a device buffer of 3*blocks");
+  cudaError_t e = launch_clock_stamp(reinterpret_cast<unsigned long long*>(device_out), blocks,
+                                     static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(TNX_ERR_CUDA, cudaGetErrorString(e));
+  return TNX_OK;
+}
+
 }  // extern "C"

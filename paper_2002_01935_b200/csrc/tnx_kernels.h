@@ -220,6 +220,7 @@ cudaError_t launch_allreduce(const double2* acc, const double2* comp, const long
 cudaError_t launch_set_counter(unsigned long long* counter, unsigned long long v, cudaStream_t st);
 cudaError_t launch_convert_c128(const double2* src, float2* dst, int64_t n, cudaStream_t st);
 cudaError_t launch_zero(void* p, int64_t bytes, cudaStream_t st);
+cudaError_t launch_clock_stamp(unsigned long long* out, int blocks, cudaStream_t st);
 
 // tcgen05 split-TF32 complex GEMM over packed planes.
 struct GemmPlan {

@@ -27,6 +27,8 @@ CONFIGS = {
                          desc="random 5-regular network, 100 tensors, bond dim 2"),
     "cfg3_lattice20": dict(make=lambda: gen.square_lattice(20, seed=0), ws=None,
                            desc="20x20 OBC square lattice, bond dim 2, scalar"),
+    "cfg3g_lattice20": dict(make=lambda: gen.square_lattice(20, seed=0), ws=None,
+                            desc="20x20 OBC square lattice, bond dim 2, scalar; plain greedy tree"),
     "cfg4_7x7_d40": dict(make=lambda: gen.grid_circuit(7, 7, 40, seed=0), ws=27,
                          desc="rectangular 7x7 (1+40+1) random circuit amplitude, 742 rank-3 tensors"),
     "cfg4g_7x7_d40": dict(make=lambda: gen.grid_circuit(7, 7, 40, seed=0), ws=27,
