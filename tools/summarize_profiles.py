@@ -55,14 +55,17 @@ def launches():
     for r in rows:
         if r.get("Metric Name") != "gpu__time_duration.sum":
             continue
-        name = r["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "").replace("tnx::", "")
+        if "Kernel Name" not in r:
+            continue
+        name = (r["Kernel Name"].replace("(anonymous namespace)::", "").replace("unnamed>::", "")
+                .split("(")[0].split("<")[0].replace("void ", "").replace("tnx::", ""))
         v = float(r["Metric Value"].replace(",", ""))
         unit = r.get("Metric Unit", "nsecond")
         tot[name] += v * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}.get(unit, 1e-6)
         cnt[name] += 1
     s = sum(tot.values())
     summ = {"command": "ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --steps 2 "
-                       "--warmup 3 --no-cpu-baseline --no-e2e --no-tf32-probe",
+                       "--warmup 3 --no-cpu-baseline --no-e2e --no-tf32-probe --sustained-s 0",
             "note": "cold-cache serialised per-launch times (bind+hoist, warmup+timed slices, profile_slice); "
                     "compare shares, not absolutes",
             "kernels": [{"kernel": k, "launches": cnt[k], "total_ms": round(tot[k], 3),
@@ -81,8 +84,7 @@ def gemm():
     t = scaled(d, units, "gpu__time_duration.sum")
     rd = scaled(d, units, "dram__bytes_read.sum")
     wr = scaled(d, units, "dram__bytes_write.sum")
-    M = N = 8192
-    K = 4096
+    M, N, K = (int(x) for x in os.environ.get("GEMM_SHAPE", "8192 8192 4096").split())
     # operand planes read once + c64 output: A 4 fp32 planes; B 4, or 6 for the
     # stacked-B instance (template argument 4 = 1: -im_hi, -im_lo planes)
     name = d["Kernel Name"]
@@ -93,7 +95,8 @@ def gemm():
     flops = 8 * M * N * K
     out = {"kernel": d["Kernel Name"],
            "command": "ncu --set full --clock-control none --import-source on -k regex:gemm_c64 -c 1 "
-                      "python tools/run_gemm.py 8192 8192 4096 1 1",
+                      f"python tools/run_gemm.py {M} {N} {K} 1 1",
+           "shape": [M, N, K],
            "sm_clock_ghz": scaled(d, units, "sm__cycles_elapsed.avg.per_second") / 1e9,
            "duration_ms": t * 1e3,
            "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
@@ -176,6 +179,7 @@ def simt():
 
 def benches():
     for src, dst in [("bench_default.log", f"{TAG}_bench_default.json"),
+                     ("bench_sustained.log", f"{TAG}_bench_long.json"),
                      ("bench_reference.log", f"{TAG}_bench_reference.json"),
                      ("bench_2rank_gloo.log", f"{TAG}_bench_2rank_gloo_shared_gpu.json")]:
         p = os.path.join(SRC, src)
