@@ -57,7 +57,7 @@ def launches():
             continue
         if "Kernel Name" not in r:
             continue
-        name = (r["Kernel Name"].replace("(anonymous namespace)::", "").replace("unnamed>::", "")
+        name = (r["Kernel Name"].replace("(anonymous namespace)::", "").replace("<unnamed>::", "").replace("unnamed>::", "")
                 .split("(")[0].split("<")[0].replace("void ", "").replace("tnx::", ""))
         v = float(r["Metric Value"].replace(",", ""))
         unit = r.get("Metric Unit", "nsecond")
