@@ -83,6 +83,13 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* tmap, uint
       : "memory");
 }
 
+// L2 prefetch of a TMA box (no shared-memory destination)
+__device__ __forceinline__ void tma_prefetch_3d(const void* tmap, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+
 // L2 policy of the operand loads: evict_last (operands are re-read by the other
 // tiles of the wave) or evict_normal (TNX_GEMM_L2HINT=0)
 __device__ __forceinline__ uint64_t l2_policy(bool keep) {
@@ -183,6 +190,8 @@ struct GemmArgs {
   float rz_kappa;        // round-toward-zero compensation (see the promotion loop); 0 disables
   int32_t l2keep;        // operand loads with an L2 evict_last policy (TNX_GEMM_L2HINT bit 0)
   int32_t stcs;          // results stored evict-first (bit 1)
+  int32_t prefetch;      // next-unit k-blocks prefetched into L2, one per k-block of the current
+                         // unit's tail (TNX_GEMM_PREFETCH; 0 off)
 };
 
 __device__ __forceinline__ int64_t map_offset(const IdxMap& m, int64_t idx) {
@@ -220,11 +229,39 @@ __device__ __forceinline__ void st_res(float* p, float v, bool cs) {
 // EPI: 0 interleaved complex64 (or split-K partials), 1 direct planes (scalar
 // stores), 2 direct planes in float4 runs (scalar fallback for edge tiles).
 // Templated so each kernel instance carries only its own store code.
+// EPI 0 stages through shared memory (`stg`, 32 rows x 80 B per warp): a warp's
+// 32 lanes hold 32 rows, so direct row stores would touch 32 lines per
+// instruction (ncu: LSU throttling, and the MMA then waited for the epilogue on
+// mid-K GEMMs); transposed 8 columns at a time, each store instruction writes
+// 8 rows x 64 contiguous bytes.
 template <int EPI, bool MIX>
 __device__ __forceinline__ void epilogue_store(const GemmArgs& g, float2* out, int64_t grow,
                                                bool row_ok, int64_t col0, int hcol,
                                                const float (&mre)[64], const float (&mim)[64],
-                                               const int64_t* gtab) {
+                                               const int64_t* gtab, unsigned char* stg) {
+  if constexpr (EPI == 0) {
+    if (col0 + 64 <= g.N && (g.N & 1) == 0 && __all_sync(0xffffffffu, row_ok)) {
+      const int lane = threadIdx.x & 31;
+      const int64_t grow0 = grow - lane;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        float4* w = reinterpret_cast<float4*>(stg + lane * 80);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          w[k] = make_float4(mre[8 * c + 2 * k], mim[8 * c + 2 * k], mre[8 * c + 2 * k + 1],
+                             mim[8 * c + 2 * k + 1]);
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = i * 8 + (lane >> 2), q = lane & 3;
+          const float4 v = *reinterpret_cast<const float4*>(stg + r * 80 + q * 16);
+          st_res(reinterpret_cast<float4*>(out + (grow0 + r) * g.N + col0 + 8 * c) + q, v, g.stcs);
+        }
+        __syncwarp();
+      }
+      return;
+    }
+  }
   if (!row_ok) return;
   if (EPI == 2 && col0 + 64 <= g.N) {
     const int64_t f = map_offset(g.fmap, grow);
@@ -350,7 +387,10 @@ struct KCfg {
   static constexpr int NSTAGE = TWO_SM && !STACK ? 4 : 3;
   static constexpr int GTAB_OFF = NSTAGE * STAGE;                      // 1 KB column table
   static constexpr int BAR_OFF = GTAB_OFF + BN * 8;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static constexpr int STG_OFF = BAR_OFF + 256;                        // EPI 0 staging: 8 warps x 2.5 KB
+  static constexpr int STG_ROW = 80;                                   // 8 complex + 16 B pad (bank spread)
+  static constexpr int STG_WARP = 32 * STG_ROW;
+  static constexpr int SMEM = STG_OFF + 8 * STG_WARP + 1024;
   static constexpr int TILE_M = TWO_SM ? 256 : BM;
 };
 
@@ -492,7 +532,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int nkb = min(g.num_kb - kb_begin, g.kb_per_split);
         const int row_a = (int)(b * g.M + (int64_t)tm * C::TILE_M + rank * BM);
         const int row_b = (int)(b * g.N + (int64_t)tn * BN + (STACK ? 0 : rank * BN_HALF));
+        // next unit (L2 prefetch of its first k-blocks, spread over this unit's tail)
+        const int un = u + ncta;
+        int z2 = 0, b2 = 0, tm2 = 0, tn2 = 0;
+        if (g.prefetch > 0 && un < units) decode_unit(g, un, z2, b2, tm2, tn2);
+        const int kb2 = z2 * g.kb_per_split;
+        const int nkb2 = min(g.num_kb - kb2, g.kb_per_split);
+        const int npf = (g.prefetch > 0 && un < units) ? min(g.prefetch, nkb2) : 0;
         for (int kb = 0; kb < nkb; ++kb) {
+          const int j = kb - (nkb - npf);
+          if (j >= 0) {
+            const bool rev = g.ksnake && (((un - cid) / ncta) & 1);
+            const int kq = kb2 + (rev ? nkb2 - 1 - j : j);
+            const int ra = (int)(b2 * g.M + (int64_t)tm2 * C::TILE_M + rank * BM);
+            const int rb = (int)(b2 * g.N + (int64_t)tn2 * BN + (STACK ? 0 : rank * BN_HALF));
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+              const int bp = STACK ? (rank == 0 ? (p < 2 ? p : p + 2) : (p < 2 ? p + 2 : p - 2)) : p;
+              tma_prefetch_3d(&tm_a, 0, ra, p * g.num_kb + kq);
+              tma_prefetch_3d(&tm_b, 0, rb, bp * g.num_kb + kq);
+            }
+          }
           mbar_wait(smem_addr(&empty[stage]), phase ^ 1u);
           const uint32_t fb = smem_addr(&full[stage]);
           if (g.debug & 1) {
@@ -719,7 +779,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         asm volatile("bar.sync 1, 256;" ::: "memory");
       }
       epilogue_store<EPI, MIX>(g, out, (int64_t)b * g.M + row, row < g.M, (int64_t)tn * BN + h * 64, h * 64, mre,
-                     mim, gtab);
+                     mim, gtab, smem + C::STG_OFF + (warp - 2) * C::STG_WARP);
     }
   }
   __syncwarp();
@@ -1028,6 +1088,8 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
     static const int l2hint = getenv("TNX_GEMM_L2HINT") ? atoi(getenv("TNX_GEMM_L2HINT")) : 1;
     a.l2keep = l2hint & 1;
     a.stcs = (l2hint >> 1) & 1;
+    static const int pf = getenv("TNX_GEMM_PREFETCH") ? atoi(getenv("TNX_GEMM_PREFETCH")) : 0;
+    a.prefetch = pf;
   }
   const int splits = g.splits > 1 ? g.splits : 1;
   a.kb_per_split = (a.num_kb + splits - 1) / splits;
