@@ -83,13 +83,6 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* tmap, uint
       : "memory");
 }
 
-// L2 prefetch of a TMA box (no shared-memory destination)
-__device__ __forceinline__ void tma_prefetch_3d(const void* tmap, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
-                   reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2)
-               : "memory");
-}
-
 // L2 policy of the operand loads: evict_last (operands are re-read by the other
 // tiles of the wave) or evict_normal (TNX_GEMM_L2HINT=0)
 __device__ __forceinline__ uint64_t l2_policy(bool keep) {
@@ -190,8 +183,6 @@ struct GemmArgs {
   float rz_kappa;        // round-toward-zero compensation (see the promotion loop); 0 disables
   int32_t l2keep;        // operand loads with an L2 evict_last policy (TNX_GEMM_L2HINT bit 0)
   int32_t stcs;          // results stored evict-first (bit 1)
-  int32_t prefetch;      // next-unit k-blocks prefetched into L2, one per k-block of the current
-                         // unit's tail (TNX_GEMM_PREFETCH; 0 off)
 };
 
 __device__ __forceinline__ int64_t map_offset(const IdxMap& m, int64_t idx) {
@@ -532,27 +523,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int nkb = min(g.num_kb - kb_begin, g.kb_per_split);
         const int row_a = (int)(b * g.M + (int64_t)tm * C::TILE_M + rank * BM);
         const int row_b = (int)(b * g.N + (int64_t)tn * BN + (STACK ? 0 : rank * BN_HALF));
-        // next unit (L2 prefetch of its first k-blocks, spread over this unit's tail)
-        const int un = u + ncta;
-        int z2 = 0, b2 = 0, tm2 = 0, tn2 = 0;
-        if (g.prefetch > 0 && un < units) decode_unit(g, un, z2, b2, tm2, tn2);
-        const int kb2 = z2 * g.kb_per_split;
-        const int nkb2 = min(g.num_kb - kb2, g.kb_per_split);
-        const int npf = (g.prefetch > 0 && un < units) ? min(g.prefetch, nkb2) : 0;
         for (int kb = 0; kb < nkb; ++kb) {
-          const int j = kb - (nkb - npf);
-          if (j >= 0) {
-            const bool rev = g.ksnake && (((un - cid) / ncta) & 1);
-            const int kq = kb2 + (rev ? nkb2 - 1 - j : j);
-            const int ra = (int)(b2 * g.M + (int64_t)tm2 * C::TILE_M + rank * BM);
-            const int rb = (int)(b2 * g.N + (int64_t)tn2 * BN + (STACK ? 0 : rank * BN_HALF));
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-              const int bp = STACK ? (rank == 0 ? (p < 2 ? p : p + 2) : (p < 2 ? p + 2 : p - 2)) : p;
-              tma_prefetch_3d(&tm_a, 0, ra, p * g.num_kb + kq);
-              tma_prefetch_3d(&tm_b, 0, rb, bp * g.num_kb + kq);
-            }
-          }
           mbar_wait(smem_addr(&empty[stage]), phase ^ 1u);
           const uint32_t fb = smem_addr(&full[stage]);
           if (g.debug & 1) {
@@ -1088,8 +1059,6 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
     static const int l2hint = getenv("TNX_GEMM_L2HINT") ? atoi(getenv("TNX_GEMM_L2HINT")) : 1;
     a.l2keep = l2hint & 1;
     a.stcs = (l2hint >> 1) & 1;
-    static const int pf = getenv("TNX_GEMM_PREFETCH") ? atoi(getenv("TNX_GEMM_PREFETCH")) : 0;
-    a.prefetch = pf;
   }
   const int splits = g.splits > 1 ? g.splits : 1;
   a.kb_per_split = (a.num_kb + splits - 1) / splits;
