@@ -106,6 +106,18 @@ def load_peaks():
 
 
 def load_traffic():
+    """DRAM traffic of the dominant tensor-core launch of a bench slice, from
+    the committed ncu launch list with dram metrics (tools/summarize_profiles.py
+    inslice_traffic); falls back to the standalone full capture."""
+    path = os.path.join(REPO, "profiles", "r02_gemm_inslice_traffic.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            t = json.load(fh)
+        d = t["dominant"]
+        return {"dram_bytes_per_launch": d["dram_bytes"], "algorithmic_bytes": d["algorithmic_bytes"],
+                "kernel": (f"gemm_c64_3xtf32 in-slice v{d['ssa']} M={d['M']} N={d['N']} K={d['K']} "
+                           f"(profiles/r02_gemm_inslice_traffic.json: {d['ratio']:.2f}x its algorithmic bytes; "
+                           f"all tensor-core launches of the slice {t['all_gemm_ratio']:.2f}x)")}
     path = os.path.join(REPO, "profiles", "ncu_gemm_traffic.json")
     if os.path.exists(path):
         with open(path) as fh:

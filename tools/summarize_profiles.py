@@ -177,6 +177,52 @@ def simt():
     print("simt:", [(k["kernel"], round(k["duration_us"], 1), round(k["achieved_gbs_algorithmic"])) for k in ks])
 
 
+def inslice_traffic():
+    """DRAM bytes of every tensor-core launch of one bench slice (ncu launch
+    list with dram metrics + the bench's --profile-out vertex list) against the
+    kernel's algorithmic bytes: operand planes read once (16 B per A element,
+    24 B per stacked-B / 16 B per B element) + the result written once (8 B
+    complex64, 16 B direct planes)."""
+    path = os.path.join(SRC, "launches_dram.csv")
+    prof_path = os.path.join(SRC, "profile.json")
+    if not (os.path.exists(path) and os.path.exists(prof_path)):
+        return
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+    h = rows[hi]
+    ki, mi, vi, ii = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
+    per, names = defaultdict(dict), {}
+    for r in rows[hi + 1:]:
+        per[int(r[ii])][r[mi]] = float(r[vi].replace(",", ""))
+        names[int(r[ii])] = r[ki]
+    prof = json.load(open(prof_path))
+    verts = {v["ssa"]: v for v in prof["vertices"]}
+    gl = [l for l in prof["launches"] if l[0] == "gemm"]
+    g_ids = [i for i in sorted(per) if "gemm_c64" in names[i]][-len(gl):]
+    out = []
+    for l, i in zip(gl, g_ids):
+        x = verts[l[1]]
+        b, m, n, k = x["batch"], x["m"], x["n"], x["k"]
+        kp = (k + 15) // 16 * 16
+        ta = names[i].split("kernel<")[1].split(">")[0].split(",")
+        epi, stacked = ta[2].strip(), ta[3].strip() == "1"
+        alg = 16 * b * m * kp + (24 if stacked else 16) * b * n * kp + (8 if epi == "0" else 16) * b * m * n
+        dram = per[i]["dram__bytes_read.sum"] + per[i]["dram__bytes_write.sum"]
+        out.append({"ssa": l[1], "M": m, "N": n, "K": k, "batch": b, "epilogue": int(epi), "stacked_b": stacked,
+                    "ms_ncu": per[i]["gpu__time_duration.sum"] / 1e6, "dram_bytes": dram, "algorithmic_bytes": alg,
+                    "ratio": dram / alg})
+    out.sort(key=lambda r: -r["ms_ncu"])
+    td, ta_ = sum(r["dram_bytes"] for r in out), sum(r["algorithmic_bytes"] for r in out)
+    summ = {"command": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,"
+                       "sm__cycles_elapsed.max --clock-control none python bench.py --steps 1 --warmup 0 "
+                       "--no-cpu-baseline --no-e2e --no-tf32-probe --sustained-s 0 --profile-out profile.json",
+            "note": "last profiled slice's tensor-core launches (cold-cache, serialised by ncu)",
+            "dominant": out[0], "all_gemm_dram_bytes": td, "all_gemm_algorithmic_bytes": ta_,
+            "all_gemm_ratio": td / ta_, "launches": out}
+    json.dump(summ, open(os.path.join(DST, f"{TAG}_gemm_inslice_traffic.json"), "w"), indent=1)
+    print("in-slice gemm traffic: dominant ratio", round(out[0]["ratio"], 2), "all", round(td / ta_, 2))
+
+
 def benches():
     for src, dst in [("bench_default.log", f"{TAG}_bench_default.json"),
                      ("bench_sustained.log", f"{TAG}_bench_long.json"),
@@ -191,6 +237,7 @@ def benches():
 if __name__ == "__main__":
     os.makedirs(DST, exist_ok=True)
     launches()
+    inslice_traffic()
     gemm()
     perm()
     simt()
