@@ -58,14 +58,19 @@ def main():
         tot_g += g
         tot_r += r
         rows.append({"slice": s, "rel": abs(g - r) / abs(r) if r else None,
+                     "bias": ((g - r) * r.conjugate()).real / abs(r) ** 2 if r else None,
                      "cond": row["scale"] / abs(r) if r else None,
                      "normwise": abs(g - r) / row["scale"] if row["scale"] else None})
     dt = time.perf_counter() - t0
     plan.close()
-    rels = [x["rel"] for x in rows if x["rel"] is not None]
+    big = max(abs(complex(*row["value"])) for row in fx["slices"])
+    nz = [x for x, row in zip(rows, fx["slices"]) if abs(complex(*row["value"])) > 1e-10 * big]
+    rows = [dict(x, zero=abs(complex(*row["value"])) <= 1e-10 * big) for x, row in zip(rows, fx["slices"])]
+    rels = [x["rel"] for x in nz]
     out = {"key": args.key, "precision": args.precision,
            "env": {k: v for k, v in os.environ.items() if k.startswith("TNX_")},
-           "n": len(rows), "max_rel": max(rels), "median_rel": sorted(rels)[len(rels) // 2],
+           "n": len(rows), "n_nonzero": len(nz), "max_rel": max(rels), "median_rel": sorted(rels)[len(rels) // 2],
+           "mean_bias": sum(x["bias"] for x in nz) / len(nz),
            "sum_rel": abs(tot_g - tot_r) / abs(tot_r), "fixture_sum_rel_vs_stored":
            abs(tot_r - complex(*fx["sum"])) / abs(complex(*fx["sum"])),
            "s_per_slice": dt / len(rows), "slices": rows}
