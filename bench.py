@@ -242,6 +242,43 @@ def run_reference(args):
     return 0
 
 
+def measure_secondary(name, torch, stream, probe, sms, W=2, K=8):
+    """A short timed run of another BASELINE workload (its default W_s, slice
+    prefix or all slices), reported beside the headline: TFLOP/s, mean SM
+    clock (cycle stamps) and the fraction of the split-TF32 ceiling at it."""
+    from paper_2002_01935_b200 import _native
+    from paper_2002_01935_b200.executor import SlicedPlan
+    from paper_2002_01935_b200.harness.workloads import load_workload
+    tn, tree, ss, meta = load_workload(name)
+    plan = SlicedPlan(tn, tree, ss).bind()
+    try:
+        ids = [i % plan.d for i in range(W + K)]
+        for s_ in ids[:W]:
+            plan.run(s_, s_ + 1, stream)
+        torch.cuda.synchronize()
+        stamps = _native.ClockStamps()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        stamps.start(stream.cuda_stream)
+        e0.record(stream)
+        for s_ in ids[W:]:
+            plan.run(s_, s_ + 1, stream)
+        e1.record(stream)
+        stamps.stop(stream.cuda_stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        mhz, _ = stamps.mhz()
+        flops = plan.flops_per_slice
+        value = K * flops / (ms / 1e3) / 1e12
+        peak = probe["tf32_flop_per_clk_per_sm"] * sms * mhz * 1e6 / 1e12 / 3.0 if probe and mhz else None
+        return {"workload": name, "desc": meta["desc"], "W": meta["W"], "log10_C": meta["log10_C"],
+                "W_s": ss.Ws, "d_sliced": str(ss.d), "flops_per_slice": flops, "steps": K,
+                "value": value, "unit": "TFLOP/s", "ms_per_step": ms / K, "slices_per_s": K / (ms / 1e3),
+                "sm_mhz_cycles": mhz, "roofline_peak": peak, "frac": value / peak if peak else None,
+                "tree_source": meta["tree_source"]}
+    finally:
+        plan.close()
+
+
 def spawn_ranks(n):
     """`bench.py --gpus N` without a launcher: start one rank per GPU under
     torch.distributed.run (127.0.0.1 rendezvous) and return its exit code.
@@ -276,6 +313,8 @@ def main():
     ap.add_argument("--slices", default="nonzero", choices=["nonzero", "prefix"],
                     help="timed slice ids: the workload's nonzero-slice list (benchdata/<config>.slices.json) "
                          "or the enumeration prefix")
+    ap.add_argument("--secondary", default="cfg5_syc53_m12",
+                    help="comma-separated workloads timed briefly after the headline ('' to skip)")
     ap.add_argument("--sustained-s", type=float, default=10.0,
                     help="after the headline, time ~this many seconds of further slices (0: skip)")
     ap.add_argument("--no-direct", action="store_true", help="disable GEMM->GEMM operand-plane fusion")
@@ -652,8 +691,7 @@ def main():
         parity = {"slice": sid, "gpu": [gpu_val.real, gpu_val.imag], "cpu": [ref_val.real, ref_val.imag],
                   "normwise_err": abs(gpu_val - ref_val) / scale if scale else None,
                   "normwise_def": "|c_gpu - c_cpu| / (||x_root|| ||y_root||), operands of the root "
-                                  "contraction from the complex128 oracle (slices of this circuit are often "
-                                  "exactly zero, so a plain relative error is undefined)",
+                                  "contraction from the complex128 oracle",
                   "rel_err": abs(gpu_val - ref_val) / abs(ref_val) if ref_val != 0 else None}
 
     if rank == 0:
@@ -691,8 +729,11 @@ def main():
                                    "ratio": value / 1.353} if args.config == WORKLOAD else None),
                 "allreduce_ms": allreduce_ms, "setup_s": setup_s, "backend": backend if use_dist else None,
                 "prefix_sum": [complex(np.asarray(total).ravel()[0]).real, complex(np.asarray(total).ravel()[0]).imag]}
-        print(json.dumps(line, default=str))
     plan.close()
+    if rank == 0:
+        if world == 1 and args.config == WORKLOAD and args.secondary:
+            line["secondary"] = [measure_secondary(name, torch, stream, probe, sms) for name in args.secondary.split(",")]
+        print(json.dumps(line, default=str))
     if use_dist:
         dist.destroy_process_group()
     return 0

@@ -176,8 +176,11 @@ struct GemmArgs {
   float* dplanes;
   int64_t dplane_stride;
   IdxMap fmap, gmap;
-  int32_t debug;         // TNX_GEMM_DEBUG bit 0: skip the TMA loads (MMA-pipeline ceiling; wrong results)
+  int32_t debug;         // TNX_GEMM_DEBUG bit 0: skip the TMA loads, bit 1: skip the epilogue stores,
+                         // bit 2 / 3: paired direct planes without the negated planes / plane 0 only
+                         // (pipeline ceilings; wrong results)
   int32_t dstack;        // direct planes of a stacked-B parent operand: also write -im_hi, -im_lo (planes 4, 5)
+  int32_t dpair;         // direct planes in full-line pairs (see epilogue_store)
   int32_t ksnake;        // odd waves traverse K in reverse (L2 reuse across waves)
   int32_t first;         // k-blocks of a unit's first TMEM round (>= promote; see launch_gemm)
   float rz_kappa;        // round-toward-zero compensation (see the promotion loop); 0 disables
@@ -249,6 +252,51 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& g, float2* out, i
           st_res(reinterpret_cast<float4*>(out + (grow0 + r) * g.N + col0 + 8 * c) + q, v, g.stcs);
         }
         __syncwarp();
+      }
+      return;
+    }
+  }
+  // EPI 1, paired lines: when 16 consecutive rows are 64 contiguous bytes of a
+  // plane and columns 2c, 2c+1 are adjacent 64 B chunks (g.dpair), lanes 0-15
+  // (rows r..r+15) and 16-31 (rows r+16..r+31) swap one value per column pair
+  // so each store instruction writes two whole 128 B lines -- half the store
+  // requests of one 64 B segment per half-warp, and the L1->crossbar request
+  // path is shared with the TMA operand loads (ncu: the mid-K GEMMs' stores
+  // starved the loads).
+  if constexpr (EPI == 1 && !MIX) {
+    if (g.dpair && col0 + 64 <= g.N && __all_sync(0xffffffffu, row_ok)) {
+      const int lane = threadIdx.x & 31;
+      const bool up = lane >= 16;
+      const int64_t f = map_offset(g.fmap, grow);
+      const int64_t fa = __shfl_sync(0xffffffffu, f, lane & 15);         // row (lane & 15)
+      const int64_t fb = __shfl_sync(0xffffffffu, f, (lane & 15) + 16);  // row (lane & 15) + 16
+      float* d = g.dplanes;
+      const int64_t ps = g.dplane_stride;
+      const int64_t sh = up ? 16 : 0;
+#pragma unroll
+      for (int j = 0; j < 64; j += 2) {
+        const int64_t oj = gtab[hcol + j];
+        float v[2][4];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          v[c][0] = tf32_hi(mre[j + c]);
+          v[c][1] = tf32_lo(mre[j + c], v[c][0]);
+          v[c][2] = tf32_hi(mim[j + c]);
+          v[c][3] = tf32_lo(mim[j + c], v[c][2]);
+        }
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const float recv = __shfl_xor_sync(0xffffffffu, up ? v[0][p] : v[1][p], 16);
+          const float a = up ? recv : v[0][p];   // line of rows 0-15: columns j | j+1
+          const float b = up ? v[1][p] : recv;   // line of rows 16-31
+          if ((g.debug & 8) && p > 0) continue;  // debug: plane 0 only
+          st_res(d + fa + oj + sh + p * ps, a, g.stcs);
+          st_res(d + fb + oj + sh + p * ps, b, g.stcs);
+          if (g.dstack && p >= 2 && !(g.debug & 4)) {  // planes 4, 5: -im_hi, -im_lo
+            st_res(d + fa + oj + sh + (p + 2) * ps, -a, g.stcs);
+            st_res(d + fb + oj + sh + (p + 2) * ps, -b, g.stcs);
+          }
+        }
       }
       return;
     }
@@ -749,6 +797,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (e < BN) gtab[e] = (cb + e < g.N) ? map_offset(g.gmap, cb + e) : 0;
         asm volatile("bar.sync 1, 256;" ::: "memory");
       }
+      if (!(g.debug & 2))
       epilogue_store<EPI, MIX>(g, out, (int64_t)b * g.M + row, row < g.M, (int64_t)tn * BN + h * 64, h * 64, mre,
                      mim, gtab, smem + C::STG_OFF + (warp - 2) * C::STG_WARP);
     }
@@ -1037,6 +1086,7 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
     static const int dbg = getenv("TNX_GEMM_DEBUG") ? atoi(getenv("TNX_GEMM_DEBUG")) : 0;
     a.debug = dbg;
     a.dstack = g.dstack;
+    a.dpair = g.dpair;
     static const int snake = getenv("TNX_GEMM_KSNAKE") ? atoi(getenv("TNX_GEMM_KSNAKE")) : 1;
     a.ksnake = snake;
     // a unit's first TMEM round spans TNX_GEMM_FIRST (default 6) k-blocks, later

@@ -40,6 +40,12 @@ static int fail(int code, const std::string& msg) {
   return code;
 }
 
+// TNX_GEMM_DPAIR=0 disables the paired full-line direct-plane stores (A/B)
+static bool dpair_off() {
+  static const int v = getenv("TNX_GEMM_DPAIR") ? atoi(getenv("TNX_GEMM_DPAIR")) : 1;
+  return v == 0;
+}
+
 #define TNX_CUDA(call)                                                                  \
   do {                                                                                  \
     cudaError_t e__ = (call);                                                           \
@@ -1074,6 +1080,19 @@ int lower(Plan& P) {
             for (int i = 0; vec && i < g.fmap.n; ++i)
               if (g.fmap.st0[i] % 4) vec = false;
             g.dvec = vec ? 1 : 0;
+            // paired full-line stores (EPI 1): rows contiguous in groups of 16 and
+            // column pairs 16 floats apart
+            const IdxMap& fm = g.fmap;
+            int64_t e = 1;
+            bool rows16 = fm.n >= 1;
+            for (int i = fm.n - 1; rows16 && i >= 0 && e < 16; --i) {
+              if (fm.st0[i] != e) rows16 = false;
+              e *= fm.dim[i];
+            }
+            const int64_t ra_rows = v.swap ? v.N : v.M;
+            g.dpair = !vec && rows16 && e >= 16 && ra_rows % 32 == 0 && gm.n >= 1 && gm.st0[gm.n - 1] == 16 &&
+                              gm.dim[gm.n - 1] % 2 == 0 && !g.mix && !dpair_off()
+                          ? 1 : 0;
           }
         }
         P.gemms.push_back(g);

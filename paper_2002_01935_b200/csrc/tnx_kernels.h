@@ -242,7 +242,8 @@ struct GemmPlan {
   int32_t dside;
   int32_t stackb;         // stacked-B 2-CTA variant: B planes carry -im_hi, -im_lo (6 planes)
   int32_t dstack;         // direct planes of a stacked-B parent's B operand (write 6 planes)
-  int32_t pad2;
+  int32_t dpair;          // direct planes: 16 consecutive rows are 64 contiguous bytes and column
+                          // pairs adjacent 64 B chunks -> full-line stores (epilogue exchanges lanes)
   float* dplanes;
   int64_t dplane_stride;
   IdxMap fmap;            // output row (batch*M + m) -> plane offset (st0)
