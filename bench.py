@@ -209,7 +209,7 @@ def run_reference(args):
     budget = args.ref_budget
     spent = 0.0
     nz_path = os.path.join(REPO, "benchdata", f"{args.config}.slices.json")
-    ids = list(range(warm + steps))
+    ids = [i % int(ss.d) for i in range(warm + steps)]  # unsliced / few-slice configs repeat
     if args.slices == "nonzero" and os.path.exists(nz_path):
         with open(nz_path) as fh:
             nz_rec = json.load(fh)
