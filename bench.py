@@ -474,46 +474,17 @@ def main():
     slices_per_s = total_slices / (ms_max / 1e3)
     timed_zero = zero_fraction(slice_values(timed_ids)) if st["out_elements"] == 1 else None
 
-    # sustained: the same per-slice work for >= --sustained-s seconds (the GEMMs
-    # run into the 1 kW power cap; the headline above is a ~0.5 s burst)
-    sustained = None
-    if args.sustained_s > 0:
-        n_s = max(K, int(math.ceil(args.sustained_s * 1e3 / (ms_max / K))))
-        s_base = world * (W + K) + rank * n_s
-        sus_ids = job_ids(s_base, n_s)
-        if use_list or cyc or s_base + n_s <= plan.d:
-            plan.reset(stream)
-            clk2 = ClockSampler(local).start()
-            barrier()
-            torch.cuda.synchronize()
-            f0 = torch.cuda.Event(enable_timing=True)
-            f1 = torch.cuda.Event(enable_timing=True)
-            stamps.start(stream.cuda_stream)
-            f0.record(stream)
-            run_ids(sus_ids)
-            f1.record(stream)
-            stamps.stop(stream.cuda_stream)
-            torch.cuda.synchronize()
-            barrier()
-            clocks2 = clk2.stop()
-            clocks2["sm_mhz_cycles"], clocks2["sm_cycle_stamps"] = stamps.mhz()
-            ms2 = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=red_dev)
-            if use_dist:
-                dist.all_reduce(ms2, op=dist.ReduceOp.MAX)
-            ms2 = float(ms2.item())
-            # a contiguous block (zero slices follow the sliced labels' digit
-            # pattern, so a strided sample can alias with it)
-            mid = max(0, n_s // 2 - 24)
-            sample = sus_ids[mid:mid + 48]
-            sustained = {"value": n_s * world * flops_slice / (ms2 / 1e3) / 1e12, "unit": "TFLOP/s",
-                         "seconds": ms2 / 1e3, "slices_per_rank": n_s, "ms_per_step": ms2 / n_s,
-                         "slices_per_s": n_s * world / (ms2 / 1e3), "clocks": clocks2,
-                         "zero_slice_fraction": zero_fraction(slice_values(sample))
-                         if st["out_elements"] == 1 else None,
-                         "zero_sample": f"{len(sample)} consecutive slices from the middle of the sustained range"}
-
     # per-launch profile of one slice (CUDA events on the launching stream)
+    # (the profile runs right after the headline, before the sustained run heats
+    # the GPU; its own mean SM clock prices the per-kernel roofline)
+    torch.cuda.synchronize()
+    stamps.start(stream.cuda_stream)
+    torch.cuda.synchronize()
     prof_b = plan.profile_slice(timed_ids[0], with_bytes=True)
+    torch.cuda.synchronize()
+    stamps.stop(stream.cuda_stream)
+    torch.cuda.synchronize()
+    prof_mhz, _ = stamps.mhz()
     prof = [(k, v, t) for k, v, t, b in prof_b]
     info = {v["ssa"]: v for v in plan.vertex_info()}
     gemm_ms = sum(t for k, v, t in prof if k == "gemm")
@@ -542,15 +513,16 @@ def main():
                       "ffma_flop_per_clk_per_sm": f_t * 1e12 / (f_mhz * 1e6) / sms})
     committed, committed_src = load_mma_peak()
     timed_mhz = clocks.get("sm_mhz_cycles") or clocks.get("sm_mhz")
-    if probe and timed_mhz:
+    prof_clock = prof_mhz or timed_mhz
+    if probe and prof_clock:
         # the probe's per-clock rate at the clock the timed slices ran at (the
         # MMA-only loop on random operands draws more power than the GEMM and
         # runs at a lower clock, so its raw TFLOP/s would understate the ceiling)
-        p_c = probe["tf32_flop_per_clk_per_sm"] * sms * timed_mhz * 1e6 / 1e12 / 3.0
+        p_c = probe["tf32_flop_per_clk_per_sm"] * sms * prof_clock * 1e6 / 1e12 / 3.0
         peak_src = (f"live tnx_mma_peak (tcgen05.mma kind::tf32 MMA-only loop, cta_group::{probe['cta_group']}): "
-                    f"{probe['tf32_flop_per_clk_per_sm']:.0f} flop/clk/SM x {sms} SMs x {timed_mhz:.0f} MHz "
-                    f"(mean SM clock over the timed slices, from clock64/globaltimer stamps) / 3 split-TF32 "
-                    f"passes; raw probe {probe['tf32_tflops']:.1f} TFLOP/s at {probe['sm_mhz']:.0f} MHz")
+                    f"{probe['tf32_flop_per_clk_per_sm']:.0f} flop/clk/SM x {sms} SMs x {prof_clock:.0f} MHz "
+                    f"(mean SM clock over the per-launch profile the achieved figure comes from, "
+                    f"clock64/globaltimer stamps) / 3 split-TF32 passes; raw probe {probe['tf32_tflops']:.1f} TFLOP/s at {probe['sm_mhz']:.0f} MHz")
     elif probe:
         p_c = probe["tf32_tflops"] / 3.0
         peak_src = (f"live tnx_mma_peak: tcgen05.mma kind::tf32 MMA-only loop, cta_group::{probe['cta_group']}, "
@@ -604,8 +576,8 @@ def main():
     # per-slice vertex -- P = the split-TF32 ceiling for tensor-core vertices, the
     # FFMA ceiling (same clock) for SIMT ones -- summed and divided by the
     # measured slice time
-    p_simt = (probe["ffma_flop_per_clk_per_sm"] * sms * timed_mhz * 1e6 / 1e12
-              if probe and timed_mhz else None)
+    p_simt = (probe["ffma_flop_per_clk_per_sm"] * sms * prof_clock * 1e6 / 1e12
+              if probe and prof_clock else None)
     t_star = 0.0
     if p_simt:
         bw = peaks["hbm_gbs"] * 1e9
@@ -633,6 +605,11 @@ def main():
                 "peak_source": peak_src,
                 "mma_probe": probe,
                 "probe_peak_raw": probe["tf32_tflops"] / 3.0 if probe else None,
+                "profile_sm_mhz_cycles": prof_mhz,
+                # the whole timed slice (every kernel, launch gaps) against the same ceiling
+                # at the timed region's own clock
+                "value_frac_at_timed_clock": (value / (probe["tf32_flop_per_clk_per_sm"] * sms * timed_mhz
+                                                       * 1e6 / 1e12 / 3.0) if probe and timed_mhz else None),
                 "measured_peaks_bf16_context": peaks["bf16_tflops"] / 2.0 / 3.0,
                 "gemm_share_of_slice": gemm_ms / slice_ms if slice_ms else None,
                 "gemm_launches_per_slice": n_gemm,
@@ -648,6 +625,44 @@ def main():
     if args.profile_out and rank == 0:
         with open(args.profile_out, "w") as fh:
             json.dump({"launches": prof, "vertices": list(info.values())}, fh, default=str)
+
+    # sustained: the same per-slice work for >= --sustained-s seconds (the GEMMs
+    # run into the 1 kW power cap; the headline above is a ~0.5 s burst)
+    sustained = None
+    if args.sustained_s > 0:
+        n_s = max(K, int(math.ceil(args.sustained_s * 1e3 / (ms_max / K))))
+        s_base = world * (W + K) + rank * n_s
+        sus_ids = job_ids(s_base, n_s)
+        if use_list or cyc or s_base + n_s <= plan.d:
+            plan.reset(stream)
+            clk2 = ClockSampler(local).start()
+            barrier()
+            torch.cuda.synchronize()
+            f0 = torch.cuda.Event(enable_timing=True)
+            f1 = torch.cuda.Event(enable_timing=True)
+            stamps.start(stream.cuda_stream)
+            f0.record(stream)
+            run_ids(sus_ids)
+            f1.record(stream)
+            stamps.stop(stream.cuda_stream)
+            torch.cuda.synchronize()
+            barrier()
+            clocks2 = clk2.stop()
+            clocks2["sm_mhz_cycles"], clocks2["sm_cycle_stamps"] = stamps.mhz()
+            ms2 = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=red_dev)
+            if use_dist:
+                dist.all_reduce(ms2, op=dist.ReduceOp.MAX)
+            ms2 = float(ms2.item())
+            # a contiguous block (zero slices follow the sliced labels' digit
+            # pattern, so a strided sample can alias with it)
+            mid = max(0, n_s // 2 - 24)
+            sample = sus_ids[mid:mid + 48]
+            sustained = {"value": n_s * world * flops_slice / (ms2 / 1e3) / 1e12, "unit": "TFLOP/s",
+                         "seconds": ms2 / 1e3, "slices_per_rank": n_s, "ms_per_step": ms2 / n_s,
+                         "slices_per_s": n_s * world / (ms2 / 1e3), "clocks": clocks2,
+                         "zero_slice_fraction": zero_fraction(slice_values(sample))
+                         if st["out_elements"] == 1 else None,
+                         "zero_sample": f"{len(sample)} consecutive slices from the middle of the sustained range"}
 
     # end-to-end through the public API: pinned host leaves -> bind -> slice -> D2H
     e2e = None

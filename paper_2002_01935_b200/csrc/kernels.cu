@@ -294,7 +294,26 @@ __global__ void __launch_bounds__(256) simt_batch_kernel(const SimtParams* __res
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
     }
-    if (valid && gl == 0) p.z[o] = acc;
+    if (valid && gl == 0) {
+      if (p.znp > 0) {
+        // SIMT -> GEMM fusion: the parent GEMM's split-TF32 operand planes
+        int64_t off = 0;
+        decode1(p.zmap, o, off);
+        float* d = p.zplanes + off;
+        const float rh = tf32_hi(acc.x), ih = tf32_hi(acc.y);
+        const float rl = tf32_lo(acc.x, rh), il = tf32_lo(acc.y, ih);
+        d[0] = rh;
+        d[p.zps] = rl;
+        d[2 * p.zps] = ih;
+        d[3 * p.zps] = il;
+        if (p.znp == 6) {
+          d[4 * p.zps] = -ih;
+          d[5 * p.zps] = -il;
+        }
+      } else {
+        p.z[o] = acc;
+      }
+    }
   }
 }
 

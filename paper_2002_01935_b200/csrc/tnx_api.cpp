@@ -40,6 +40,12 @@ static int fail(int code, const std::string& msg) {
   return code;
 }
 
+// TNX_SIMT_PLANES=0 disables the SIMT -> GEMM operand-plane fusion (A/B)
+static bool simt_planes_off() {
+  static const int v = getenv("TNX_SIMT_PLANES") ? atoi(getenv("TNX_SIMT_PLANES")) : 1;
+  return v == 0;
+}
+
 // TNX_GEMM_DPAIR=0 disables the paired full-line direct-plane stores (A/B)
 static bool dpair_off() {
   static const int v = getenv("TNX_GEMM_DPAIR") ? atoi(getenv("TNX_GEMM_DPAIR")) : 1;
@@ -122,6 +128,8 @@ struct Vertex {
   int two_sm = 0;                   // 2-CTA GEMM configuration
   bool stack = false;               // stacked-B variant (B planes carry -im_hi, -im_lo)
   bool swap = false;  // GEMM A operand taken from y (larger row count)
+  int plane_parent = -1;            // batched SIMT writes the parent GEMM's operand planes
+  int plane_side = -1;
   int direct_parent = -1;           // GEMM writes the parent's operand planes
   int direct_side = -1;
   bool side_direct[2] = {false, false};  // operand planes written by a child GEMM
@@ -766,6 +774,35 @@ int compile(Plan& P, const tnx_plan_desc* D) {
       }
     }
   }
+  // SIMT -> GEMM fusion: a small contraction (batched thread / warp mode) whose
+  // parent is a GEMM writes its result straight into the parent's K-blocked
+  // split-TF32 operand planes (no materialised tensor, no pack launch).  Its
+  // output elements cover the planes exactly (K is not padded: plane_order).
+  if (P.precision == TNX_PREC_3XTF32 && !(P.flags & TNX_FLAG_NO_DIRECT) &&
+      !(P.flags & TNX_FLAG_STRIP_EXPONENT) && !simt_planes_off()) {
+    for (int k = 0; k < P.n - 1; ++k) {
+      Vertex& pv = P.V[k];
+      if (pv.kind != VK_GEMM) continue;
+      for (int side = 0; side < 2; ++side) {
+        if (pv.side_direct[side]) continue;
+        const int c = side == 0 ? (pv.swap ? pv.b : pv.a) : (pv.swap ? pv.a : pv.b);
+        if (c < P.n) continue;
+        Vertex& cv = P.V[c - P.n];
+        if ((cv.kind != VK_SIMT_T && cv.kind != VK_SIMT_W) || cv.hoisted != pv.hoisted) continue;
+        std::vector<int> dst;
+        if (!plane_order(P, pv, side, dst)) continue;
+        cv.plane_parent = pv.ssa;
+        cv.plane_side = side;
+        pv.side_direct[side] = true;
+        const int ph = pv.hoisted ? 0 : 1;
+        Block& pb = P.blocks[ph][side == 0 ? pv.blk_apl : pv.blk_bpl];
+        pb.first = std::min(pb.first, step[c]);
+        TensorLoc& tc = P.T[c];
+        if (tc.arena == AR_WORK && tc.block >= 0) P.blocks[ph][tc.block].bytes = kAlign;
+        tc.fused = true;
+      }
+    }
+  }
   if (getenv("TNX_DEBUG_PLAN")) {
     for (auto& v : P.V) {
       if (v.kind != VK_GEMM) continue;
@@ -1143,6 +1180,20 @@ int lower(Plan& P) {
         s.partial = P.partial;
         s.sum_tab = v.tab_off >= 0 ? P.d_tabs + v.tab_off : nullptr;
         s.group_lg = v.kind == VK_SIMT_W ? 5 : 0;
+        if (v.plane_parent >= 0) {
+          const Vertex& pv = P.V[v.plane_parent - P.n];
+          std::vector<int> pdst;
+          if (!plane_order(P, pv, v.plane_side, pdst))
+            return fail(TNX_ERR_INVALID, "simt planes: parent layout changed");
+          TensorLoc pl;
+          pl.labels = pdst;
+          if (!build_map(P, z.labels, &pl, nullptr, s.zmap, err))
+            return fail(TNX_ERR_INVALID, "vertex " + std::to_string(v.ssa) + ": " + err);
+          const int64_t pra = pv.swap ? pv.N : pv.M, prb = pv.swap ? pv.M : pv.N;
+          s.zplanes = reinterpret_cast<float*>(P.block_ptr(phase, v.plane_side == 0 ? pv.blk_apl : pv.blk_bpl));
+          s.zps = pv.B * (v.plane_side == 0 ? pra : prb) * pv.kp;
+          s.znp = v.plane_side == 1 && pv.stack ? 6 : 4;
+        }
         if (v.kind == VK_SIMT_T && s.sum.n == 1 && v.sum_size >= 2 &&
             (s.sum.st0[0] == 1 || s.sum.st1[0] == 1)) {
           // the summed run is contiguous in an operand: 2^lg lanes per output read it coalesced

@@ -69,13 +69,17 @@ struct SimtParams {
   int32_t nsplit;
   int32_t mode;
   int32_t group_lg;       // batched THREAD/WARP: 2^group_lg lanes per output (0 thread ... 5 warp)
-  int32_t pad;
+  int32_t znp;            // > 0: the result is written as znp split-TF32 operand planes of the
+                          // parent GEMM (4, or 6 for a stacked-B operand) instead of z
+  float* zplanes;         // plane 0 of the parent's operand (stride zps floats per plane)
+  int64_t zps;
+  IdxMap zmap;            // output index -> offset in a plane (st0)
 };
 
 // Pack a complex64 tensor into fp32 planes [re_hi, re_lo, im_hi, im_lo]
 // (+ [-im_hi, -im_lo] when nplanes == 6, the GEMM B operand), each
-// [rows][kp] (rows = batch*R, K padded to kp with zeros); hi = tf32
-// truncation, lo = x - hi.
+// [rows][kp] (rows = batch*R, K padded to kp with zeros); hi = x rounded to
+// nearest TF32, lo = (x - hi) rounded to nearest TF32.
 struct PackParams {
   IdxMap row;             // row index -> src offset (st0)
   IdxMap col;             // k index (k < K) -> src offset (st0)
