@@ -4,17 +4,22 @@
     python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference]
 
 One "step" = one slice of BASELINE.json configs[3] (rectangular 7x7 (1+40+1)
-random-circuit amplitude, 742 rank-3 tensors, reference-driver tree, sliced by
-greedy_slice to W_s = 27) per GPU: every rank contracts its own contiguous
-block of slice ids (weak scaling, no data-path collective); the per-rank
-complex128 partial sums meet in one NCCL all-reduce at the end.
+random-circuit amplitude, 742 rank-3 tensors, reference min-fill tree, sliced
+by greedy_slice to W_s = 27) per GPU.  The timed slices are drawn from the
+workload's list of slices that are nonzero in exact arithmetic
+(benchdata/cfg4_7x7_d40.slices.json, found by tools/slice_scan.py); every rank
+contracts its own block of that list (weak scaling, no data-path collective)
+and the per-rank complex128 partial sums meet in one NCCL all-reduce.
 
 Metric: effective contraction FLOP/s = 8 * C_s(executed) / t,
 reported in TFLOP/s, whole job over all ranks, with slices/s alongside.
 Inputs are resident in HBM for `value`; `e2e` re-binds the leaves from pinned
 host memory and reads the result back every step through the public API.
-The per-slice working set (5+ GiB of intermediates) exceeds the 126 MB L2, so
-no explicit L2 flush is needed between timed slices.
+Also in the line: the roofline against the measured tensor-pipe ceiling at the
+measured SM clock, a >= 10 s sustained run, the CPU oracle on one slice with
+the slice's parity, and a short run of configs[4] (`secondary`).  The
+per-slice working set (11 GB of intermediates) exceeds the 126 MB L2, so no
+explicit L2 flush is needed between timed slices.
 """
 
 from __future__ import annotations
