@@ -44,8 +44,10 @@ typedef enum {
 typedef enum {
   TNX_PREC_FP32 = 0,     /* every contraction on FP32 SIMT kernels */
   TNX_PREC_3XTF32 = 1,   /* GEMM-shaped contractions on tcgen05 tensor cores,
-                            split-TF32 (hi*hi + hi*lo + lo*hi), 4M complex,
-                            FP32 accumulation in TMEM; the rest FP32 SIMT */
+                            split-TF32 (hi*hi + hi*lo + lo*hi, hi and lo rounded
+                            to nearest), 4M complex, FP32 accumulation in TMEM
+                            promoted every 3 k-blocks with round-toward-zero
+                            compensation; the rest FP32 SIMT */
   TNX_PREC_TF32_BF16X = 2 /* as 3XTF32 but the two small cross terms hi*lo +
                             lo*hi run as BF16 MMAs (2x tensor rate, ~2^-20
                             relative per product) */
