@@ -15,6 +15,7 @@ seeded networks, trees and slice sets and compare against the stored values.
   exact arithmetic).
 * ``d40r`` -- 8 seeded picks from the rest of that list.
 * ``d40g`` / ``d40gr`` -- the same for the greedy-driver tree (cfg4g).
+* ``syc``  -- slices 0..7 of configs[4] (Sycamore-53 m=12, W_s=27).
 
 Per slice it stores the value, its root-operand scale ||x|| ||y|| (the
 condition of the last contraction) and the slice's label assignment digits, so
@@ -45,6 +46,8 @@ SETS = {
     # the same circuit under the greedy-driver tree (round-1 bench workload)
     "d40g": ("cfg4g_7x7_d40", 27, list(range(16))),
     "d40gr": ("cfg4g_7x7_d40", 27, "random8"),
+    # BASELINE configs[4]: Sycamore-like 53-qubit m=12 amplitude (synthetic fSim)
+    "syc": ("cfg5_syc53_m12", 27, list(range(8))),
 }
 
 
