@@ -46,7 +46,7 @@ def test_nonzero_slice_list_matches_the_slice_set():
     assert all(0 <= s < ss.d for s in ids)
 
 
-@pytest.mark.parametrize("key", ["d24", "d40", "d40r", "d40g", "d40gr"])
+@pytest.mark.parametrize("key", ["d24", "d40", "d40r", "d40g", "d40gr", "syc"])
 def test_northstar_fixture_matches_the_slicer(key):
     from paper_2002_01935_b200.harness.workloads import load_workload
     from paper_2002_01935_b200.slicing import slice_assignment

@@ -1,6 +1,6 @@
 """North-star parity (BASELINE.json north_star):
-the sliced 7x7 (1+40+1) circuit amplitude workload and the full 7x7 (1+24+1)
-amplitude, GPU (default precision: split-TF32 tensor cores + FP32 SIMT,
+the sliced 7x7 (1+40+1) circuit amplitude workload, the full 7x7 (1+24+1)
+amplitude and 8 slices of the Sycamore-53 m=12 amplitude (configs[4]), GPU (default precision: split-TF32 tensor cores + FP32 SIMT,
 complex64 storage) against complex128 oracle values.
 
 The oracle needs ~20 s per d40 slice on 16 cores, so its values are committed
@@ -61,7 +61,7 @@ def _run(key):
     return fx, got, total
 
 
-@pytest.mark.parametrize("key", ["d40", "d40r", "d40g", "d40gr", "d24"])
+@pytest.mark.parametrize("key", ["d40", "d40r", "d40g", "d40gr", "d24", "syc"])
 def test_northstar_slices(key):
     if key not in FIX:
         pytest.fail(f"fixture {key} missing: run tests/golden/make_circuit_fixtures.py {key}")
