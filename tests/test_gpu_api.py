@@ -155,3 +155,30 @@ def test_cli_strip_exponent(tmp_path, capsys):
     assert abs(np.log10(abs(val)) + doc["exponent10"] - (np.log10(abs(ref0)) + 240)) < 1e-5
     # without the flag the value overflows: exit code 5 (numeric)
     assert main([str(tmp_path / "n.json"), str(tmp_path / "p.json")]) == 5
+
+
+def test_measurement_diagnostics():
+    """tnx_mma_peak (the roofline denominator) and tnx_clock_stamp (the clock
+    the roofline is priced at) return physically plausible numbers."""
+    import torch
+    from paper_2002_01935_b200 import _native as nat
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    for kind, cg, per_clk in (("tf32", 2, 4096), ("tf32", 1, 4096), ("bf16", 2, 8192), ("ffma", 1, 256)):
+        t, mhz, ms = nat.mma_peak(kind, cg, 20000)
+        assert 300 <= mhz <= 2500, (kind, mhz)
+        rate = t * 1e12 / (mhz * 1e6) / sms  # flop per clock per SM
+        assert 0.85 * per_clk <= rate <= 1.02 * per_clk, (kind, cg, rate)
+        assert ms > 0
+    with pytest.raises(ValueError):
+        nat.mma_peak("tf32", 3, 20000)
+    st = torch.cuda.Stream()
+    stamps = nat.ClockStamps()
+    stamps.start(st.cuda_stream)
+    with torch.cuda.stream(st):
+        a = torch.randn(4096, 4096, device="cuda")
+        for _ in range(20):
+            a = a @ a * 1e-2
+    stamps.stop(st.cuda_stream)
+    torch.cuda.synchronize()
+    mhz, n = stamps.mhz()
+    assert n >= sms // 2 and 300 <= mhz <= 2500, (mhz, n)
