@@ -403,15 +403,9 @@ def main():
     timed_ids = job_ids(rank * (W + K) + W if use_list else base + W, K)
 
     def run_ids(ids):
-        """Contract `ids` into the accumulator: contiguous runs go through one
-        tnx_run_slices call (graph replays), others one call per id."""
-        i = 0
-        while i < len(ids):
-            j = i + 1
-            while j < len(ids) and ids[j] == ids[j - 1] + 1:
-                j += 1
-            plan.run(ids[i], ids[j - 1] + 1, stream)
-            i = j
+        """Contract `ids` into the accumulator in one library call
+        (tnx_run_slice_ids: consecutive runs replay the graph back to back)."""
+        plan.run_ids(ids, stream)
     red_dev = "cuda" if backend == "nccl" else "cpu"
 
     def barrier():

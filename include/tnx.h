@@ -142,6 +142,12 @@ int tnx_bind_leaves(void* plan, const void* const* leaf_data, int32_t dtype,
  * into the device accumulator.  Asynchronous on `stream`. */
 int tnx_run_slices(void* plan, uint64_t s_begin, uint64_t s_end, void* stream);
 
+/* Contract the slices ids[0..n) (any order, repeats allowed; each < d) and
+ * add them into the accumulator, like tnx_run_slices over each id; runs of
+ * consecutive ids replay the per-slice graph back to back.  The id-list form
+ * of SPEC contract_sliced(..., slice_ids) and of sampled-slice runs. */
+int tnx_run_slice_ids(void* plan, const uint64_t* ids, int64_t n, void* stream);
+
 int tnx_reset_accumulator(void* plan, void* stream);
 
 /* Copy the accumulator (complex128 interleaved, tn.output order) to host;

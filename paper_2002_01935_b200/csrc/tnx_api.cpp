@@ -1548,6 +1548,37 @@ int tnx_run_slices(void* plan, uint64_t s_begin, uint64_t s_end, void* stream) {
   return mark_done(P, st);
 }
 
+int tnx_run_slice_ids(void* plan, const uint64_t* ids, int64_t n, void* stream) {
+  if (!plan) return fail(TNX_ERR_INVALID, "null plan");
+  Plan& P = *static_cast<Plan*>(plan);
+  if (!P.bound) return fail(TNX_ERR_STATE, "tnx_run_slice_ids before tnx_bind_leaves");
+  if (n < 0 || (n > 0 && !ids)) return fail(TNX_ERR_INVALID, "tnx_run_slice_ids: bad id list");
+  for (int64_t i = 0; i < n; ++i)
+    if ((u128)ids[i] >= P.d) return fail(TNX_ERR_INVALID, "slice id " + std::to_string(ids[i]) + " out of [0, d)");
+  TNX_CUDA(cudaSetDevice(P.device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.own;
+  if (n == 0) return TNX_OK;
+  if (int orc = order_after(P, st)) return orc;
+  // maximal runs of consecutive ids: one counter write, then graph replays
+  // (the last kernel of each replay advances the device-side slice id)
+  for (int64_t i = 0; i < n;) {
+    int64_t j = i + 1;
+    while (j < n && ids[j] == ids[j - 1] + 1) ++j;
+    cudaError_t e = launch_set_counter(P.counter, ids[i], st);
+    if (e != cudaSuccess) return fail(TNX_ERR_CUDA, cudaGetErrorString(e));
+    for (int64_t k = i; k < j; ++k) {
+      if (P.gexec) {
+        TNX_CUDA(cudaGraphLaunch(P.gexec, st));
+      } else {
+        int rc = run_launches(P, P.slice_launches, st, -1);
+        if (rc) return rc;
+      }
+    }
+    i = j;
+  }
+  return mark_done(P, st);
+}
+
 int tnx_reset_accumulator(void* plan, void* stream) {
   Plan& P = *static_cast<Plan*>(plan);
   if (!P.bound) return fail(TNX_ERR_STATE, "not bound");

@@ -259,6 +259,15 @@ class SlicedPlan:
         nat.check(self._lib.tnx_run_slices(self._h, int(s_begin), int(s_end), self._stream(stream)))
         return self
 
+    def run_ids(self, ids, stream=None):
+        """Contract the slices in ``ids`` (an iterable of ids in [0, d), any
+        order) into the accumulator in one library call (tnx_run_slice_ids)."""
+        if not self._bound:
+            raise ValueError("bind() leaf data before run_ids()")
+        arr = (C.c_uint64 * max(1, len(ids)))(*[int(s) for s in ids])
+        nat.check(self._lib.tnx_run_slice_ids(self._h, arr, len(ids), self._stream(stream)))
+        return self
+
     def reset(self, stream=None):
         nat.check(self._lib.tnx_reset_accumulator(self._h, self._stream(stream)))
 

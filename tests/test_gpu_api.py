@@ -182,3 +182,30 @@ def test_measurement_diagnostics():
     torch.cuda.synchronize()
     mhz, n = stamps.mhz()
     assert n >= sms // 2 and 300 <= mhz <= 2500, (mhz, n)
+
+
+def test_run_slice_ids_matches_ranges():
+    """tnx_run_slice_ids (any order, repeats, consecutive runs) sums exactly
+    what the equivalent ranges do; out-of-range ids raise ValueError."""
+    tn = gen.grid_circuit(4, 5, 12, seed=11)
+    tree = refpkg.greedy_sample(tn, 1.0, 0.0, 0)
+    ss = greedy_slice(tree, tn, refpkg.metrics(tree, tn).width - 4, restarts=1)
+    plan = SlicedPlan(tn, tree, ss).bind()
+    try:
+        d = plan.d
+        ids = [3, 4, 5, 0, 9 % d, 3]
+        plan.reset()
+        plan.run_ids(ids)
+        got = complex(plan.result())
+        plan.reset()
+        for s in ids:
+            plan.run(s, s + 1)
+        ref = complex(plan.result())
+        assert got == ref, (got, ref)
+        with pytest.raises(ValueError):
+            plan.run_ids([0, d])
+        plan.reset()
+        plan.run_ids([])
+        assert complex(plan.result()) == 0
+    finally:
+        plan.close()
