@@ -177,8 +177,8 @@ struct GemmArgs {
   int64_t dplane_stride;
   IdxMap fmap, gmap;
   int32_t debug;         // TNX_GEMM_DEBUG bit 0: skip the TMA loads, bit 1: skip the epilogue stores,
-                         // bit 2 / 3: paired direct planes without the negated planes / plane 0 only
-                         // (pipeline ceilings; wrong results)
+                         // bit 2 / 3: paired direct planes without the negated planes / plane 0 only,
+                         // bit 5: no MMAs (pipeline ceilings; wrong results)
   int32_t dstack;        // direct planes of a stacked-B parent operand: also write -im_hi, -im_lo (planes 4, 5)
   int32_t dpair;         // direct planes in full-line pairs (see epilogue_store)
   int32_t ksnake;        // odd waves traverse K in reverse (L2 reuse across waves)
@@ -656,6 +656,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const uint64_t bi_h = umma_desc_sw64(bb + 2 * C::B_BYTES);
               const uint64_t bi_l = umma_desc_sw64(bb + 3 * C::B_BYTES);
               const uint32_t acc0 = (kb > kb0 || ks > 0) ? 1u : 0u;
+              if (g.debug & 32) continue;  // debug: no MMAs (operand-streaming ceiling)
               if constexpr (STACK) {
                 // slots: 0 [re_hi | im_hi], 1 [re_lo | im_lo], 2 [-im_hi | re_hi], 3 [-im_lo | re_lo]
                 umma_tf32_2sm(d_re, ar_h, br_l, ID_S, acc0);  // hi.lo
