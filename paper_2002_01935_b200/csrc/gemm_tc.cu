@@ -1147,7 +1147,9 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t st) {
   }
   cfg.attrs = attr;
   if (g.two_sm) {
-    const int64_t clusters = std::min<int64_t>(units, 74);
+    // TNX_GEMM_MAXPAIRS caps the persistent grid (diagnostics: per-SM vs chip-wide limits)
+    static const int64_t maxpairs = getenv("TNX_GEMM_MAXPAIRS") ? atoll(getenv("TNX_GEMM_MAXPAIRS")) : 74;
+    const int64_t clusters = std::min<int64_t>(units, std::max<int64_t>(1, std::min<int64_t>(74, maxpairs)));
     cfg.gridDim = dim3((unsigned)(2 * clusters));
     cfg.dynamicSmemBytes = g.stackb ? KCfg<true, true>::SMEM : KCfg<true>::SMEM;
     attr[nattr].id = cudaLaunchAttributeClusterDimension;
