@@ -154,6 +154,12 @@ int tnx_reset_accumulator(void* plan, void* stream);
  * synchronises `stream`.  out_elems must equal stats.out_elements. */
 int tnx_partial_result(void* plan, double* out, int64_t out_elems, void* stream);
 
+/* As tnx_partial_result but asynchronous: the copy is enqueued on `stream`
+ * and the call returns; `out` (pinned host memory for a true async copy)
+ * holds the result once the stream has been synchronised.  Lets a caller
+ * pipeline bind -> run -> read over many steps without a host sync each. */
+int tnx_partial_result_async(void* plan, double* out, int64_t out_elems, void* stream);
+
 /* strip_exponent plans: per output element value = out * 2^exp2. */
 int tnx_partial_result_exp(void* plan, double* out, int64_t* exp2, int64_t out_elems, void* stream);
 

@@ -66,6 +66,7 @@ SIGNATURES = {
     "tnx_run_slice_ids": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.c_int64, C.c_void_p]),
     "tnx_reset_accumulator": (C.c_int, [C.c_void_p, C.c_void_p]),
     "tnx_partial_result": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_int64, C.c_void_p]),
+    "tnx_partial_result_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "tnx_partial_result_exp": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int64,
                                          C.c_void_p]),
     "tnx_stats_get": (C.c_int, [C.c_void_p, C.POINTER(Stats)]),

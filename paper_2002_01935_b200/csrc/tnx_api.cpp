@@ -1601,6 +1601,17 @@ int tnx_partial_result(void* plan, double* out, int64_t out_elems, void* stream)
   return TNX_OK;
 }
 
+int tnx_partial_result_async(void* plan, double* out, int64_t out_elems, void* stream) {
+  Plan& P = *static_cast<Plan*>(plan);
+  if (!P.bound) return fail(TNX_ERR_STATE, "not bound");
+  if (out_elems != P.out_size) return fail(TNX_ERR_INVALID, "output size mismatch");
+  if (!out) return fail(TNX_ERR_INVALID, "null output buffer");
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.own;
+  if (int orc = order_after(P, st)) return orc;
+  TNX_CUDA(cudaMemcpyAsync(out, P.acc, P.out_size * 16, cudaMemcpyDeviceToHost, st));
+  return mark_done(P, st);
+}
+
 int tnx_partial_result_exp(void* plan, double* out, int64_t* exp2, int64_t out_elems, void* stream) {
   Plan& P = *static_cast<Plan*>(plan);
   if (!P.bound) return fail(TNX_ERR_STATE, "not bound");

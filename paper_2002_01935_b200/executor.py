@@ -279,6 +279,25 @@ class SlicedPlan:
         val = (buf[0::2] + 1j * buf[1::2])[:n].reshape(self.out_shape)
         return val
 
+    def result_async(self, out, stream=None):
+        """Enqueue the accumulator's copy into ``out`` (a caller-owned buffer of
+        2 * out_elements float64 -- pinned host memory, e.g. a pinned torch
+        tensor -- given as an object with ``data_ptr()``, a numpy array or an
+        address) and return at once; ``out`` holds the complex128 values once
+        the stream is synchronised."""
+        n = int(self._stats.out_elements)
+        if hasattr(out, "data_ptr"):
+            if out.numel() < 2 * max(n, 1):
+                raise ValueError("result_async buffer too small")
+            ptr = out.data_ptr()
+        elif hasattr(out, "ctypes"):
+            if out.size < 2 * max(n, 1):
+                raise ValueError("result_async buffer too small")
+            ptr = out.ctypes.data
+        else:
+            ptr = int(out)
+        nat.check(self._lib.tnx_partial_result_async(self._h, C.c_void_p(ptr), n, self._stream(stream)))
+
     def profile_slice(self, s=0, with_bytes=False):
         """Per-launch CUDA-event timings of one (non-accumulated) slice:
         list of (kind, ssa vertex, ms[, algorithmic bytes])."""

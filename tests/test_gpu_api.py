@@ -209,3 +209,25 @@ def test_run_slice_ids_matches_ranges():
         assert complex(plan.result()) == 0
     finally:
         plan.close()
+
+
+def test_result_async_matches_result():
+    """tnx_partial_result_async enqueues the read; after a stream sync the
+    buffer equals tnx_partial_result's value."""
+    import torch
+    tn = gen.grid_circuit(4, 4, 10, seed=5)
+    tree = refpkg.greedy_sample(tn, 1.0, 0.0, 0)
+    ss = greedy_slice(tree, tn, refpkg.metrics(tree, tn).width - 2, restarts=1)
+    plan = SlicedPlan(tn, tree, ss).bind()
+    try:
+        st = torch.cuda.Stream()
+        buf = torch.zeros(2, dtype=torch.float64).pin_memory()
+        plan.run(0, plan.d, st)
+        plan.result_async(buf, st)
+        st.synchronize()
+        ref = complex(plan.result(st))
+        assert complex(buf[0].item(), buf[1].item()) == ref
+        with pytest.raises(ValueError):
+            plan.result_async(torch.zeros(1, dtype=torch.float64).pin_memory(), st)
+    finally:
+        plan.close()
