@@ -625,6 +625,40 @@ def main():
         with open(args.profile_out, "w") as fh:
             json.dump({"launches": prof, "vertices": list(info.values())}, fh, default=str)
 
+    # end-to-end through the public API: pinned host leaves -> bind -> slice -> D2H
+    e2e = None
+    if not args.no_e2e:
+        leaves = []
+        for nid in tree.leaves:
+            a = torch.from_numpy(np.ascontiguousarray(tn.node(nid).data, dtype=np.complex128)).pin_memory()
+            leaves.append(a.numpy())
+        h2d = sum(a.nbytes for a in leaves)
+        nout = max(1, st["out_elements"])
+        d2h = 16 * nout
+        res = torch.zeros((len(timed_ids), 2 * nout), dtype=torch.float64).pin_memory()
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        # every step: H2D of the leaves (bind), the slice, and an async D2H of the
+        # step's result into pinned host memory; one synchronisation at the end
+        for i, sid_ in enumerate(timed_ids):
+            plan.bind(leaf_arrays=leaves, stream=stream)
+            plan.run(sid_, sid_ + 1, stream)
+            plan.result_async(res[i], stream)
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        if not bool(torch.isfinite(res).all()):
+            raise SystemExit("e2e: non-finite step result")
+        t_e = torch.tensor([e2e_s], dtype=torch.float64, device=red_dev)
+        if use_dist:
+            dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
+        e2e_s = float(t_e.item())
+        e2e = {"value": total_slices * flops_slice / e2e_s / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "slices_per_s": total_slices / e2e_s,
+               "note": "each step: tnx_bind_leaves (H2D from pinned host + slice-invariant subtrees) + 1 slice "
+                       "+ async D2H of the step's result into pinned host memory; one sync at the end"}
+
     # sustained: the same per-slice work for >= --sustained-s seconds (the GEMMs
     # run into the 1 kW power cap; the headline above is a ~0.5 s burst)
     sustained = None
@@ -662,40 +696,6 @@ def main():
                          "zero_slice_fraction": zero_fraction(slice_values(sample))
                          if st["out_elements"] == 1 else None,
                          "zero_sample": f"{len(sample)} consecutive slices from the middle of the sustained range"}
-
-    # end-to-end through the public API: pinned host leaves -> bind -> slice -> D2H
-    e2e = None
-    if not args.no_e2e:
-        leaves = []
-        for nid in tree.leaves:
-            a = torch.from_numpy(np.ascontiguousarray(tn.node(nid).data, dtype=np.complex128)).pin_memory()
-            leaves.append(a.numpy())
-        h2d = sum(a.nbytes for a in leaves)
-        nout = max(1, st["out_elements"])
-        d2h = 16 * nout
-        res = torch.zeros((len(timed_ids), 2 * nout), dtype=torch.float64).pin_memory()
-        barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        # every step: H2D of the leaves (bind), the slice, and an async D2H of the
-        # step's result into pinned host memory; one synchronisation at the end
-        for i, sid_ in enumerate(timed_ids):
-            plan.bind(leaf_arrays=leaves, stream=stream)
-            plan.run(sid_, sid_ + 1, stream)
-            plan.result_async(res[i], stream)
-        torch.cuda.synchronize()
-        e2e_s = time.perf_counter() - t0
-        if not bool(torch.isfinite(res).all()):
-            raise SystemExit("e2e: non-finite step result")
-        t_e = torch.tensor([e2e_s], dtype=torch.float64, device=red_dev)
-        if use_dist:
-            dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
-        e2e_s = float(t_e.item())
-        e2e = {"value": total_slices * flops_slice / e2e_s / 1e12, "unit": "TFLOP/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "slices_per_s": total_slices / e2e_s,
-               "note": "each step: tnx_bind_leaves (H2D from pinned host + slice-invariant subtrees) + 1 slice "
-                       "+ async D2H of the step's result into pinned host memory; one sync at the end"}
 
     cpu = None
     parity = None
